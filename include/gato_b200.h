@@ -1,0 +1,181 @@
+/*
+ * gato_b200.h -- C ABI of the B200-native batched SQP trajectory-optimisation solve.
+ *
+ * Drop-in boundary for the reference package's batched-solve path (paths relative to
+ * /root/reference/pkg/src/trajbatch/):
+ *
+ *   gato_create / gato_bind / gato_solve      replace  batch_solve          batch.py:102-124
+ *                                             (M x sqp_solve                sqp.py:204-295)
+ *   gato_step_many                            replaces dynamics.step_many           dynamics.py:805-816
+ *   gato_step_jacobians_many                  replaces dynamics.step_jacobians_many dynamics.py:774-802
+ *   gato_pcg_batched                          replaces blocktri.pcg / btmv          blocktri.py:105-173
+ *   gato_shift_warm_start                     replaces mpc.shift_warm_start         mpc.py:85-89
+ *
+ * The reference is pure Python and has no FFI of its own; INTEGRATION.md shows the ctypes
+ * stub a maintainer would add to trajbatch/batch.py to call this library.
+ *
+ * Conventions
+ *   - plain C, no torch / C++ types; every pointer in gato_buffers and in the operator
+ *     entry points is a DEVICE pointer owned by the caller (the library never frees them);
+ *   - all floating point data is IEEE binary64, C-contiguous, packed by solve then knot
+ *     (blocktri.py:5-6);
+ *   - every call is asynchronous on the given stream (a cudaStream_t passed as void*),
+ *     never synchronises the host, and returns 0 or a negative GATO_E_* code; the text of
+ *     the last error is kept per handle (gato_last_error) -- nothing is thrown across the ABI;
+ *   - a handle is not thread safe: one handle per (device, stream).
+ */
+#ifndef GATO_B200_H
+#define GATO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GATO_ABI_VERSION 1
+
+/* model ids: the reference's analytic models (dynamics.py:145,190,255,388) + iiwa14 */
+#define GATO_MODEL_DOUBLE_INTEGRATOR 0 /* params: [dims, mass]                                 */
+#define GATO_MODEL_PENDULUM 1          /* params: [mass, length, gravity, damping]             */
+#define GATO_MODEL_CARTPOLE 2          /* params: [cart_mass, pole_mass, pole_length, gravity] */
+#define GATO_MODEL_TWO_LINK_ARM 3      /* params: [m1, m2, l1, l2, gravity, joint_damping]     */
+#define GATO_MODEL_IIWA14 4            /* params: none (table frozen in model_iiwa14.cuh)       */
+
+/* error codes */
+#define GATO_OK 0
+#define GATO_E_INVALID -1     /* bad argument / unsupported dimension */
+#define GATO_E_CUDA -2        /* CUDA runtime error (see gato_last_error) */
+#define GATO_E_UNBOUND -3     /* gato_solve before gato_bind */
+#define GATO_E_NOMEM -4
+
+/* per-solve status words written to gato_buffers.info[:, GATO_INFO_STATUS] */
+#define GATO_STATUS_OK 0
+#define GATO_STATUS_FACTORIZATION 1 /* errors.FactorizationError (errors.py:12) */
+#define GATO_STATUS_PCG_BREAKDOWN 2 /* errors.PcgBreakdownError  (errors.py:24) */
+
+/* which block failed to factor (info[:, GATO_INFO_FAIL_BLOCK]) */
+#define GATO_BLOCK_Q 0 /* "Q_{knot}"                 qpform.py:305-309 */
+#define GATO_BLOCK_R 1 /* "R_{knot}"                 qpform.py:310-311 */
+#define GATO_BLOCK_S 2 /* "S diagonal block {knot}"  qpform.py:352-353 */
+
+/* layout of the int32 info row of one solve */
+#define GATO_INFO_WORDS 8
+#define GATO_INFO_N_RECORDS 0  /* number of IterationRecords written (len(trace))       */
+#define GATO_INFO_CONVERGED 1  /* SqpResult.converged                                   */
+#define GATO_INFO_STATUS 2     /* GATO_STATUS_*                                         */
+#define GATO_INFO_FAIL_ITER 3  /* SQP iteration of the failure                          */
+#define GATO_INFO_FAIL_KNOT 4  /* FactorizationError.knot                               */
+#define GATO_INFO_FAIL_BLOCK 5 /* GATO_BLOCK_*                                          */
+#define GATO_INFO_FAIL_AUX 6   /* failing pivot (factorization) / PCG iteration (breakdown) */
+#define GATO_INFO_RETRIES 7    /* breakdown count of the failing iteration              */
+
+/* layout of one fp64 trace row == one sqp.IterationRecord (sqp.py:81-92) */
+#define GATO_TRACE_WORDS 8
+#define GATO_TRACE_MERIT 0
+#define GATO_TRACE_CONSTRAINT_L1 1
+#define GATO_TRACE_ALPHA 2 /* NaN encodes alpha=None (tolerance exit, sqp.py:261-272) */
+#define GATO_TRACE_RHO 3
+#define GATO_TRACE_PCG_ITERATIONS 4
+#define GATO_TRACE_ACCEPTED 5
+#define GATO_TRACE_STEP_INF_NORM 6
+#define GATO_TRACE_ITERATION 7
+
+typedef struct gato_config {
+  int32_t abi_version; /* GATO_ABI_VERSION */
+  int32_t model_id;
+  int32_t batch;       /* M */
+  int32_t horizon;     /* N (stage knots); X has N+1 rows */
+  int32_t state_dim;   /* n, checked against the model */
+  int32_t control_dim; /* m */
+  int32_t force_dim;   /* fdim */
+  /* sqp.SolverSettings (sqp.py:56-77) */
+  int32_t max_sqp_iterations;
+  int32_t pcg_max_iterations; /* 0 => 10 * (N+1) * n (blocktri.py:78-81) */
+  int32_t num_shrinks;        /* candidates = num_shrinks + 1 (sqp.py:39-52) */
+  int32_t regularize_r;
+  int32_t pcg_retry_limit;
+  int32_t loop_mode; /* 0 auto, 1 CUDA-graph WHILE node, 2 graph of unrolled passes, 3 plain stream launches */
+  int32_t reserved0;
+  double timestep;
+  double pcg_tolerance;
+  double mu;
+  double beta;
+  double rho_min;
+  double rho_max;
+  double rho_factor;
+  double step_tolerance; /* NaN => None: run the fixed budget (sqp.py:65-66) */
+  double feasibility_tolerance;
+  double model_params[8];
+} gato_config;
+
+/* Device buffers of one batch. Inputs are read-only for the library; X, U are in/out. */
+typedef struct gato_buffers {
+  const double* x_start;  /* [M, n]                                   qpform.py:88   */
+  const double* goal;     /* [M, N+1, n] (single goals pre-broadcast) qpform.py:66   */
+  const double* Q;        /* [M, n, n]                                qpform.py:45   */
+  const double* R;        /* [M, m, m]                                               */
+  const double* QN;       /* [M, n, n]                                               */
+  const double* force;    /* [M, N, fdim] sampled at k*h              qpform.py:113-123 */
+  const double* rho_init; /* [M]                                      batch.py:63-74 */
+  double* X;              /* [M, N+1, n] initial guess in, solution out */
+  double* U;              /* [M, N, m]                                  */
+  double* trace;          /* [M, max_sqp_iterations, GATO_TRACE_WORDS]  */
+  int32_t* info;          /* [M, GATO_INFO_WORDS]                       */
+} gato_buffers;
+
+typedef struct gato_handle gato_handle;
+
+/* Allocates the per-batch scratch (A, B, e, S, D^-1, gamma, lambda, dX, dU, merits ...)
+ * once for (M, N, n, m) on the current device. */
+int gato_create(const gato_config* cfg, gato_handle** out);
+int gato_bind(gato_handle* h, const gato_buffers* bufs);
+/* Runs every solve of the batch to termination, entirely on the device. */
+int gato_solve(gato_handle* h, void* stream);
+/* X <- [X[1:], X[-1]], U <- [U[1:], U[-1]] for every solve, in place (mpc.py:85-89). */
+int gato_shift_warm_start(gato_handle* h, void* stream);
+/* Loop modes 2/3 enqueue exactly max_sqp_iterations passes; a PCG-breakdown retry (sqp.py:240-248)
+ * consumes a pass without advancing its solve. gato_pending synchronises the stream and reports
+ * how many solves are still active; gato_resume enqueues further passes. In loop mode 1 (WHILE
+ * graph node) the device loops until every solve has terminated and pending is always 0. */
+int gato_pending(gato_handle* h, void* stream, int32_t* pending);
+int gato_resume(gato_handle* h, void* stream, int32_t passes);
+int gato_loop_mode(const gato_handle* h);
+/* Device pointer + element count of an internal stage array, for stage-by-stage parity
+ * tests: "A","B","e","grad","hinv","Sdiag","Soff","Dinv","gamma","lam","dX","dU","merits",
+ * "viols","state","pcg_iters". Valid until gato_destroy. */
+int gato_scratch(gato_handle* h, const char* name, void** dev_ptr, int64_t* count);
+/* synchronous device->host copy of the first `bytes` bytes of a stage array (tests) */
+int gato_read_scratch(gato_handle* h, const char* name, void* host_dst, int64_t bytes);
+/* number of kernel launches issued by the last gato_solve (graph nodes count per replay) */
+int64_t gato_launch_count(const gato_handle* h);
+/* device time of the last gato_solve in milliseconds, measured with CUDA events on the
+ * launching stream; synchronises on the end event */
+int gato_last_solve_ms(gato_handle* h, float* ms);
+const char* gato_last_error(const gato_handle* h);
+void gato_destroy(gato_handle* h);
+
+/* ---- operator entry points (stateless; same kernels as the solve) ---- */
+
+/* out[r] = one RK4 step of model from (X[r], U[r]) under force F[r], rows independent. */
+int gato_step_many(int32_t model_id, const double* model_params, int64_t rows, const double* X,
+                   const double* U, const double* F, double timestep, double* out, void* stream);
+/* A[r] (n x n), B[r] (n x m): exact Jacobians of the RK4 map at row r. */
+int gato_step_jacobians_many(int32_t model_id, const double* model_params, int64_t rows,
+                             const double* X, const double* U, const double* F, double timestep,
+                             double* A, double* B, void* stream);
+/* Batched PCG on explicit block-tridiagonal S and preconditioner Phi^-1 (both stored as
+ * diag [nb, bd, bd] + sub-diagonal [nb-1, bd, bd] blocks per system). status: 0 ok,
+ * 2 breakdown (iters = breakdown iteration). */
+int gato_pcg_batched(int32_t systems, int32_t n_blockrows, int32_t block_dim, const double* S_diag,
+                     const double* S_off, const double* gamma, const double* P_diag,
+                     const double* P_off, double tolerance, int32_t max_iterations, double* lam,
+                     int32_t* iterations, int32_t* converged, int32_t* status, double* residual,
+                     void* stream);
+
+const char* gato_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GATO_B200_H */

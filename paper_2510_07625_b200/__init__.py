@@ -1,0 +1,27 @@
+"""gato-b200: B200-native batched SQP trajectory optimisation (GATO, arXiv 2510.07625).
+
+Public surface mirrors the hot-path names of the reference package ``trajbatch``
+(/root/reference/pkg/src/trajbatch/__init__.py): problem and settings types, ``batch_solve``,
+``sqp_solve`` and the row-wise dynamics / PCG operators, all executed by hand-written CUDA
+kernels behind the C ABI in include/gato_b200.h.  There is no CPU execution path.
+"""
+
+from .batch import BatchSpec, batch_solve, clear_engine_cache, shard_bounds, sqp_solve
+from .engine import BatchEngine, PackedBatch, PackedResult, pcg_batched, step_jacobians_many, step_many
+from .errors import (BackendUnavailableError, ConfigError, DimensionError, FactorizationError,
+                     PcgBreakdownError)
+from .models import Cartpole, DoubleIntegrator, DynamicsModel, Iiwa14, Pendulum, TwoLinkArm
+from .problem import CostSpec, ExternalForce, ProblemSpec
+from .results import BatchResult, IterationRecord, SqpResult
+from .settings import LineSearchSettings, PcgSettings, SolverSettings
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BackendUnavailableError", "BatchEngine", "BatchResult", "BatchSpec", "Cartpole", "ConfigError",
+    "CostSpec", "DimensionError", "DoubleIntegrator", "DynamicsModel", "ExternalForce",
+    "FactorizationError", "Iiwa14", "IterationRecord", "LineSearchSettings", "PackedBatch",
+    "PackedResult", "PcgBreakdownError", "PcgSettings", "Pendulum", "ProblemSpec", "SolverSettings",
+    "SqpResult", "TwoLinkArm", "batch_solve", "clear_engine_cache", "pcg_batched", "shard_bounds",
+    "sqp_solve", "step_jacobians_many", "step_many",
+]

@@ -1,0 +1,269 @@
+// Model-independent kernels of the SQP pass (included by gato_api.cu only).
+#pragma once
+#include "solver_kernels.cuh"
+
+namespace gato {
+
+// -----------------------------------------------------------------------------------------
+// k_init: per-solve state (sqp.py:222-229).  merit_current is filled by a line-search pass
+// at alpha = 0 followed by k_init_merit.
+// -----------------------------------------------------------------------------------------
+__global__ void k_init(SolveParams P) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) {
+    P.counters[0] = 0;
+    P.counters[1] = 0;
+    P.counters[2] = (unsigned)P.M;
+    P.counters[3] = 0;
+  }
+  if (b >= P.M) return;
+  P.sd[b * SD_WORDS + SD_RHO] = P.rho_init[b];
+  P.sd[b * SD_WORDS + SD_MERIT] = 0.0;
+  P.sd[b * SD_WORDS + SD_VIOL] = 0.0;
+  P.sd[b * SD_WORDS + SD_STEP_INF] = 0.0;
+  int32_t* si = P.si + b * SI_WORDS;
+  si[SI_ACTIVE] = 1;
+  si[SI_IT] = 0;
+  si[SI_RETRIES] = 0;
+  si[SI_SKIP_LS] = 0;
+  si[SI_PCG_ITS] = 0;
+  si[SI_MERIT_VALID] = 0;
+  si[SI_SCHUR_FAIL] = INT_MAX;
+  int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
+#pragma unroll
+  for (int i = 0; i < GATO_INFO_WORDS; ++i) info[i] = 0;
+  info[GATO_INFO_FAIL_KNOT] = -1;
+}
+
+__global__ void k_init_merit(SolveParams P) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.M) return;
+  P.sd[b * SD_WORDS + SD_MERIT] = P.merits[(size_t)b * P.C];
+  P.si[b * SI_WORDS + SI_MERIT_VALID] = 1;
+}
+
+// -----------------------------------------------------------------------------------------
+// k_update: per solve: first-minimum argmin over the candidates, strict-decrease accept test
+// (sqp.py:193-195), X += a dX, U += a dU (sqp.py:277-281), IterationRecord (sqp.py:283-292),
+// adapt_rho (sqp.py:198-201), budget termination; counts the still-active solves and, when
+// run inside the WHILE graph node, sets its condition.
+// -----------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_update(SolveParams P, int nx, int nu, cudaGraphConditionalHandle cond,
+                                                int use_cond) {
+  const int b = blockIdx.x;
+  int32_t* si = P.si + b * SI_WORDS;
+  __shared__ double s_alpha;
+  __shared__ int s_accept;
+  const int active = si[SI_ACTIVE];
+  const int skip = si[SI_SKIP_LS];
+  if (active && !skip) {
+    if (threadIdx.x == 0) {
+      const double* mer = P.merits + (size_t)b * P.C;
+      int best = 0;
+      double bm = mer[0];
+      for (int c = 1; c < P.C; ++c)
+        if (mer[c] < bm) {
+          bm = mer[c];
+          best = c;
+        }
+      // np.argmin returns the first NaN if any; merits are never NaN (non-finite -> +inf)
+      const double cur = P.sd[b * SD_WORDS + SD_MERIT];
+      const int accepted = bm < cur;
+      const double alpha = P.alphas[best];
+      s_alpha = alpha;
+      s_accept = accepted;
+      double viol = P.sd[b * SD_WORDS + SD_VIOL];
+      double merit = cur;
+      if (accepted) {
+        merit = bm;
+        viol = P.viols[(size_t)b * P.C + best];
+        P.sd[b * SD_WORDS + SD_MERIT] = bm;
+      }
+      const int it = si[SI_IT];
+      const double rho = P.sd[b * SD_WORDS + SD_RHO];
+      double* tr = P.trace + ((size_t)b * P.max_it + it) * GATO_TRACE_WORDS;
+      tr[GATO_TRACE_MERIT] = merit;
+      tr[GATO_TRACE_CONSTRAINT_L1] = viol;
+      tr[GATO_TRACE_ALPHA] = alpha;
+      tr[GATO_TRACE_RHO] = rho;
+      tr[GATO_TRACE_PCG_ITERATIONS] = (double)si[SI_PCG_ITS];
+      tr[GATO_TRACE_ACCEPTED] = accepted ? 1.0 : 0.0;
+      tr[GATO_TRACE_STEP_INF_NORM] = P.sd[b * SD_WORDS + SD_STEP_INF];
+      tr[GATO_TRACE_ITERATION] = (double)it;
+      const double nrho = accepted ? rho / P.rho_factor : rho * P.rho_factor;
+      P.sd[b * SD_WORDS + SD_RHO] = fmin(fmax(nrho, P.rho_min), P.rho_max);
+      int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
+      info[GATO_INFO_N_RECORDS] = it + 1;
+      si[SI_IT] = it + 1;
+      if (it + 1 >= P.max_it) si[SI_ACTIVE] = 0;
+    }
+    __syncthreads();
+    if (s_accept) {
+      const double alpha = s_alpha;
+      const int nX = (P.N + 1) * nx, nU = P.N * nu;
+      double* X = P.X + (size_t)b * nX;
+      const double* dX = P.dX + (size_t)b * nX;
+      for (int i = threadIdx.x; i < nX; i += blockDim.x) X[i] = __dadd_rn(X[i], __dmul_rn(alpha, dX[i]));
+      double* U = P.U + (size_t)b * nU;
+      const double* dU = P.dU + (size_t)b * nU;
+      for (int i = threadIdx.x; i < nU; i += blockDim.x) U[i] = __dadd_rn(U[i], __dmul_rn(alpha, dU[i]));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int still = si[SI_ACTIVE];
+    if (still) atomicAdd(&P.counters[0], 1u);
+    __threadfence();
+    const unsigned ticket = atomicAdd(&P.counters[1], 1u);
+    if (ticket == gridDim.x - 1) {
+      __threadfence();
+      const unsigned n_active = atomicExch(&P.counters[0], 0u);
+      P.counters[1] = 0;
+      P.counters[2] = n_active;  // host-visible "pending" word
+      P.counters[3] += 1;        // passes executed
+      if (use_cond) cudaGraphSetConditional(cond, n_active > 0 ? 1u : 0u);
+    }
+  }
+}
+
+// mpc.py:85-89: shift one knot left, duplicate the tail.  One CTA per solve.
+__global__ void k_shift(double* X, double* U, int N, int nx, int nu) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.x;
+  double* Xb = X + (size_t)b * (N + 1) * nx;
+  double* Ub = U + (size_t)b * N * nu;
+  const int nX = (N + 1) * nx, nU = N * nu;
+  for (int i = threadIdx.x; i < nX; i += blockDim.x) sh[i] = Xb[i];
+  for (int i = threadIdx.x; i < nU; i += blockDim.x) sh[nX + i] = Ub[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < nX; i += blockDim.x) {
+    const int src = (i + nx < nX) ? i + nx : i;
+    Xb[i] = sh[src];
+  }
+  for (int i = threadIdx.x; i < nU; i += blockDim.x) {
+    const int src = (i + nu < nU) ? i + nu : i;
+    Ub[i] = sh[nX + src];
+  }
+}
+
+// -----------------------------------------------------------------------------------------
+// k_pcg_explicit: operator-level drop-in for blocktri.pcg (blocktri.py:123-173) on arbitrary
+// block-tridiagonal S and explicit preconditioner Phi^-1 in global memory, any block size.
+// One CTA per system, one thread per row (strided).  Keeps the reference's true-residual stop
+// test (blocktri.py:165).  Dynamic shared memory: 6 vectors of `size` doubles + 64 double2.
+// -----------------------------------------------------------------------------------------
+__device__ __forceinline__ double bt_row(const double* __restrict__ diag, const double* __restrict__ off, int nb,
+                                         int bd, const double* __restrict__ v, int row) {
+  const int k = row / bd, i = row % bd;
+  const double* D = diag + (size_t)k * bd * bd + i * bd;
+  const double* vk = v + k * bd;
+  double acc = 0.0;
+  for (int j = 0; j < bd; ++j) acc = fma(D[j], vk[j], acc);
+  if (k > 0) {
+    const double* O = off + (size_t)(k - 1) * bd * bd + i * bd;
+    const double* vm = v + (k - 1) * bd;
+    double s = 0.0;
+    for (int j = 0; j < bd; ++j) s = fma(O[j], vm[j], s);
+    acc += s;
+  }
+  if (k < nb - 1) {
+    const double* O = off + (size_t)k * bd * bd;
+    const double* vn = v + (k + 1) * bd;
+    double s = 0.0;
+    for (int j = 0; j < bd; ++j) s = fma(O[j * bd + i], vn[j], s);
+    acc += s;
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_pcg_explicit(int nb, int bd, const double* Sd, const double* So,
+                                                      const double* gamma, const double* Pd, const double* Po,
+                                                      double tol, int cap, double* lam_out, int32_t* iters,
+                                                      int32_t* converged, int32_t* status, double* residual) {
+  extern __shared__ __align__(16) double pe_smem[];
+  const int sys = blockIdx.x, size = nb * bd;
+  const size_t dstride = (size_t)nb * bd * bd, ostride = (size_t)(nb > 1 ? nb - 1 : 0) * bd * bd;
+  Sd += sys * dstride;
+  Pd += sys * dstride;
+  So += sys * ostride;
+  Po += sys * ostride;
+  gamma += (size_t)sys * size;
+  double* lam = pe_smem;
+  double* r = lam + size;
+  double* z = r + size;
+  double* p = z + size;
+  double* q = p + size;
+  double* tmp = q + size;
+  double2* red = reinterpret_cast<double2*>(tmp + size + (size & 1));
+  BlockReducer R{red, 0, (int)((blockDim.x + 31) >> 5)};
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < size; i += blockDim.x) {
+    lam[i] = 0.0;
+    r[i] = gamma[i];
+    acc += r[i] * r[i];
+  }
+  double res = sqrt(R.sum2(acc, 0.0).x);
+  int its = 0, conv = 0, st = 0;
+  if (res <= tol) {
+    conv = 1;
+  } else {
+    __syncthreads();
+    acc = 0.0;
+    for (int i = threadIdx.x; i < size; i += blockDim.x) {
+      z[i] = bt_row(Pd, Po, nb, bd, r, i);
+      p[i] = z[i];
+      acc += r[i] * z[i];
+    }
+    double rz = R.sum2(acc, 0.0).x;
+    for (int it = 1; it <= cap; ++it) {
+      __syncthreads();
+      acc = 0.0;
+      for (int i = threadIdx.x; i < size; i += blockDim.x) {
+        q[i] = bt_row(Sd, So, nb, bd, p, i);
+        acc += p[i] * q[i];
+      }
+      const double curv = R.sum2(acc, 0.0).x;
+      if (curv <= 0.0) {
+        st = GATO_STATUS_PCG_BREAKDOWN;
+        its = it;
+        break;
+      }
+      const double a = rz / curv;
+      for (int i = threadIdx.x; i < size; i += blockDim.x) {
+        lam[i] = lam[i] + a * p[i];
+        r[i] = r[i] - a * q[i];
+      }
+      __syncthreads();
+      acc = 0.0;
+      for (int i = threadIdx.x; i < size; i += blockDim.x) {
+        const double d = bt_row(Sd, So, nb, bd, lam, i) - gamma[i];
+        acc += d * d;
+      }
+      res = sqrt(R.sum2(acc, 0.0).x);
+      its = it;
+      if (res <= tol) {
+        conv = 1;
+        break;
+      }
+      acc = 0.0;
+      for (int i = threadIdx.x; i < size; i += blockDim.x) {
+        tmp[i] = bt_row(Pd, Po, nb, bd, r, i);
+        acc += r[i] * tmp[i];
+      }
+      const double rzn = R.sum2(acc, 0.0).x;
+      const double beta = rzn / rz;
+      for (int i = threadIdx.x; i < size; i += blockDim.x) p[i] = tmp[i] + beta * p[i];
+      rz = rzn;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < size; i += blockDim.x) lam_out[(size_t)sys * size + i] = lam[i];
+  if (threadIdx.x == 0) {
+    iters[sys] = its;
+    converged[sys] = conv;
+    status[sys] = st;
+    residual[sys] = res;
+  }
+}
+
+}  // namespace gato

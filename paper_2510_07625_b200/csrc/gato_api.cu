@@ -1,0 +1,466 @@
+// C ABI of the B200-native batched SQP solve (include/gato_b200.h).
+// Host-side orchestration only: scratch allocation, model dispatch, CUDA-graph construction.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common_kernels.cuh"
+#include "model_ops.cuh"
+
+using namespace gato;
+
+namespace {
+
+
+#define CK(call)                                                                               \
+  do {                                                                                         \
+    cudaError_t err__ = (call);                                                                \
+    if (err__ != cudaSuccess) {                                                                \
+      set_error(h, std::string(#call) + ": " + cudaGetErrorString(err__));                     \
+      return GATO_E_CUDA;                                                                      \
+    }                                                                                          \
+  } while (0)
+
+bool select_ops(int model_id, const double* params, ModelOps* ops) {
+  switch (model_id) {
+    case GATO_MODEL_DOUBLE_INTEGRATOR: {
+      const int dims = params ? (int)params[0] : 0;
+      if (dims == 1) *ops = gato_ops_double_integrator(1);
+      else if (dims == 2) *ops = gato_ops_double_integrator(2);
+      else if (dims == 7) *ops = gato_ops_double_integrator(7);
+      else return false;
+      return true;
+    }
+    case GATO_MODEL_PENDULUM: *ops = gato_ops_pendulum(); return true;
+    case GATO_MODEL_CARTPOLE: *ops = gato_ops_cartpole(); return true;
+    case GATO_MODEL_TWO_LINK_ARM: *ops = gato_ops_two_link_arm(); return true;
+    case GATO_MODEL_IIWA14: *ops = gato_ops_iiwa14(); return true;
+    default: return false;
+  }
+}
+
+struct Scratch {
+  const char* name;
+  void* ptr;
+  int64_t count;
+};
+
+}  // namespace
+
+struct gato_handle {
+  gato_config cfg;
+  ModelOps ops;
+  SolveParams P;
+  bool bound = false;
+  int loop_mode = 1;
+  std::vector<void*> allocs;
+  std::vector<Scratch> scratch;
+  std::string error;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphConditionalHandle cond = 0;
+  bool graph_valid = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t launches = 0;
+  int static_launches = 0;  // launches outside the pass loop
+};
+
+namespace {
+
+void set_error(gato_handle* h, const std::string& msg) {
+  if (h) h->error = msg;
+}
+void set_error(std::nullptr_t, const std::string&) {}
+
+template <class T>
+int dev_alloc(gato_handle* h, const char* name, T** out, int64_t count) {
+  void* p = nullptr;
+  const size_t bytes = (size_t)(count > 0 ? count : 1) * sizeof(T);
+  cudaError_t err = cudaMalloc(&p, bytes);
+  if (err != cudaSuccess) {
+    set_error(h, std::string("cudaMalloc(") + name + "): " + cudaGetErrorString(err));
+    return GATO_E_NOMEM;
+  }
+  cudaMemset(p, 0, bytes);
+  h->allocs.push_back(p);
+  h->scratch.push_back({name, p, count});
+  *out = static_cast<T*>(p);
+  return GATO_OK;
+}
+
+// one SQP pass: six launches
+int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond) {
+  const SolveParams& P = h->P;
+  RowView V{P.X, P.U, P.force, P.N, P.si};
+  CK(h->ops.hessinv(P, s));
+  CK(h->ops.linearize(V, P.mp, P.h, (int64_t)P.M * P.N, P.A, P.B, P.e, s));
+  CK(h->ops.schur(P, s));
+  CK(h->ops.pcg(P, s));
+  CK(h->ops.linesearch(P, 0, s));
+  k_update<<<P.M, 128, 0, s>>>(P, h->ops.nx, h->ops.nu, h->cond, use_cond);
+  CK(cudaGetLastError());
+  return GATO_OK;
+}
+
+int enqueue_prologue(gato_handle* h, cudaStream_t s) {
+  const SolveParams& P = h->P;
+  k_init<<<(P.M + 127) / 128, 128, 0, s>>>(P);
+  CK(cudaGetLastError());
+  CK(h->ops.linesearch(P, 1, s));
+  k_init_merit<<<(P.M + 127) / 128, 128, 0, s>>>(P);
+  CK(cudaGetLastError());
+  return GATO_OK;
+}
+
+void destroy_graph(gato_handle* h) {
+  if (h->exec) cudaGraphExecDestroy(h->exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  h->exec = nullptr;
+  h->graph = nullptr;
+  h->graph_valid = false;
+}
+
+// prologue -> WHILE(any solve active) { pass }
+int build_while_graph(gato_handle* h, cudaStream_t s) {
+  destroy_graph(h);
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_prologue(h, s);
+  if (rc != GATO_OK) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(s, &junk);
+    if (junk) cudaGraphDestroy(junk);
+    return rc;
+  }
+  cudaStreamCaptureStatus status;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CK(cudaStreamGetCaptureInfo_v2(s, &status, nullptr, &g, &deps, &ndeps));
+  CK(cudaGraphConditionalHandleCreate(&h->cond, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h->cond;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, ndeps, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  CK(cudaStreamEndCapture(s, &h->graph));
+  // body
+  CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  rc = enqueue_pass(h, s, 1);
+  cudaGraph_t body_out = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(s, &body_out);
+  if (rc != GATO_OK) return rc;
+  CK(e2);
+  CK(cudaGraphInstantiate(&h->exec, h->graph, 0));
+  h->graph_valid = true;
+  return GATO_OK;
+}
+
+int build_unrolled_graph(gato_handle* h, cudaStream_t s) {
+  destroy_graph(h);
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_prologue(h, s);
+  for (int it = 0; rc == GATO_OK && it < h->P.max_it; ++it) rc = enqueue_pass(h, s, 0);
+  cudaError_t e2 = cudaStreamEndCapture(s, &h->graph);
+  if (rc != GATO_OK) return rc;
+  CK(e2);
+  CK(cudaGraphInstantiate(&h->exec, h->graph, 0));
+  h->graph_valid = true;
+  return GATO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gato_version(void) { return "gato_b200 0.1 (sm_100a, fp64)"; }
+
+int gato_create(const gato_config* cfg, gato_handle** out) {
+  if (!cfg || !out) return GATO_E_INVALID;
+  *out = nullptr;
+  if (cfg->abi_version != GATO_ABI_VERSION) return GATO_E_INVALID;
+  gato_handle* h = new gato_handle();
+  h->cfg = *cfg;
+  *out = h;  // returned even on failure so that gato_last_error is readable; caller destroys
+  if (!select_ops(cfg->model_id, cfg->model_params, &h->ops)) {
+    set_error(h, "unknown model id or unsupported model dimension");
+    return GATO_E_INVALID;
+  }
+  const int nx = h->ops.nx, nu = h->ops.nu, nf = h->ops.nf;
+  if (cfg->state_dim != nx || cfg->control_dim != nu || cfg->force_dim != nf) {
+    set_error(h, "state/control/force dimensions do not match the model");
+    return GATO_E_INVALID;
+  }
+  if (cfg->batch < 1 || cfg->horizon < 1 || cfg->max_sqp_iterations < 1 || cfg->num_shrinks < 0 ||
+      !(cfg->timestep > 0.0)) {
+    set_error(h, "batch, horizon, max_sqp_iterations must be >= 1 and timestep > 0");
+    return GATO_E_INVALID;
+  }
+  if ((cfg->horizon + 1) * (nx / 2) > 1024) {
+    set_error(h, "horizon too long: (N+1)*n/2 must be <= 1024 rows-pairs per solve");
+    return GATO_E_INVALID;
+  }
+  SolveParams& P = h->P;
+  memset(&P, 0, sizeof(P));
+  const int64_t M = cfg->batch, N = cfg->horizon, nb = N + 1;
+  P.M = (int)M;
+  P.N = (int)N;
+  P.max_it = cfg->max_sqp_iterations;
+  P.pcg_cap = cfg->pcg_max_iterations > 0 ? cfg->pcg_max_iterations : (int)(10 * nb * nx);
+  P.C = cfg->num_shrinks + 1;
+  P.regularize_r = cfg->regularize_r;
+  P.retry_limit = cfg->pcg_retry_limit;
+  P.h = cfg->timestep;
+  P.pcg_tol = cfg->pcg_tolerance;
+  P.mu = cfg->mu;
+  P.rho_min = cfg->rho_min;
+  P.rho_max = cfg->rho_max;
+  P.rho_factor = cfg->rho_factor;
+  P.step_tol = cfg->step_tolerance;
+  P.feas_tol = cfg->feasibility_tolerance;
+  for (int i = 0; i < 8; ++i) P.mp.v[i] = cfg->model_params[i];
+
+  int rc = GATO_OK;
+#define ALLOC(field, count)                                                   \
+  if (rc == GATO_OK) rc = dev_alloc(h, #field, &P.field, (int64_t)(count));
+  ALLOC(A, M * N * nx * nx);
+  ALLOC(B, M * N * nx * nu);
+  ALLOC(e, M * N * nx);
+  ALLOC(grad, M * nb * (nx + nu));
+  ALLOC(hinv, M * hinv_stride(nx, nu));
+  ALLOC(Sdiag, M * nb * nx * nx);
+  ALLOC(Soff, M * N * nx * nx);
+  ALLOC(Dinv, M * nb * (nx * (nx + 1) / 2));
+  ALLOC(gamma, M * nb * nx);
+  ALLOC(lam, M * nb * nx);
+  ALLOC(dX, M * nb * nx);
+  ALLOC(dU, M * N * nu);
+  ALLOC(merits, M * P.C);
+  ALLOC(viols, M * P.C);
+  ALLOC(alphas, P.C);
+  ALLOC(sd, M * SD_WORDS);
+  ALLOC(si, M * SI_WORDS);
+  ALLOC(pcg_iters, M * P.max_it);
+  ALLOC(counters, 8);
+#undef ALLOC
+  if (rc != GATO_OK) return rc;
+  // step lengths beta^-c, computed on the host exactly as sqp.py:51-52 (libm pow)
+  std::vector<double> alphas(P.C);
+  for (int c = 0; c < P.C; ++c) alphas[c] = pow(cfg->beta, -(double)c);
+  CK(cudaMemcpy(P.alphas, alphas.data(), P.C * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaEventCreate(&h->ev0));
+  CK(cudaEventCreate(&h->ev1));
+  CK(h->ops.prepare(P));
+  h->loop_mode = cfg->loop_mode ? cfg->loop_mode : env_int("GATO_LOOP_MODE", 1);
+  return GATO_OK;
+}
+
+int gato_bind(gato_handle* h, const gato_buffers* b) {
+  if (!h || !b) return GATO_E_INVALID;
+  if (!b->x_start || !b->goal || !b->Q || !b->R || !b->QN || !b->force || !b->rho_init || !b->X || !b->U ||
+      !b->trace || !b->info) {
+    set_error(h, "gato_bind: null buffer");
+    return GATO_E_INVALID;
+  }
+  SolveParams& P = h->P;
+  const bool same = h->bound && P.x_start == b->x_start && P.goal == b->goal && P.Q == b->Q && P.R == b->R &&
+                    P.QN == b->QN && P.force == b->force && P.rho_init == b->rho_init && P.X == b->X &&
+                    P.U == b->U && P.trace == b->trace && P.info == b->info;
+  P.x_start = b->x_start;
+  P.goal = b->goal;
+  P.Q = b->Q;
+  P.R = b->R;
+  P.QN = b->QN;
+  P.force = b->force;
+  P.rho_init = b->rho_init;
+  P.X = b->X;
+  P.U = b->U;
+  P.trace = b->trace;
+  P.info = b->info;
+  h->bound = true;
+  if (!same) h->graph_valid = false;
+  return GATO_OK;
+}
+
+int gato_solve(gato_handle* h, void* stream) {
+  if (!h) return GATO_E_INVALID;
+  if (!h->bound) {
+    set_error(h, "gato_solve before gato_bind");
+    return GATO_E_UNBOUND;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int mode = h->loop_mode;
+  if ((mode == 1 || mode == 2) && !h->graph_valid) {
+    // graph capture needs a capturable stream; the legacy default stream is not
+    cudaStream_t cs = s;
+    bool own = false;
+    if (cs == nullptr || cs == cudaStreamLegacy) {
+      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      own = true;
+    }
+    int rc = (mode == 1) ? build_while_graph(h, cs) : build_unrolled_graph(h, cs);
+    if (rc != GATO_OK && mode == 1) {
+      // WHILE nodes unavailable: fall back to the unrolled graph
+      cudaGetLastError();
+      h->loop_mode = mode = 2;
+      rc = build_unrolled_graph(h, cs);
+    }
+    if (own) cudaStreamDestroy(cs);
+    if (rc != GATO_OK) {
+      cudaGetLastError();
+      h->loop_mode = mode = 3;
+    }
+  }
+  CK(cudaEventRecord(h->ev0, s));
+  if (mode == 1 || mode == 2) {
+    CK(cudaGraphLaunch(h->exec, s));
+  } else {
+    int rc = enqueue_prologue(h, s);
+    for (int it = 0; rc == GATO_OK && it < h->P.max_it; ++it) rc = enqueue_pass(h, s, 0);
+    if (rc != GATO_OK) return rc;
+  }
+  CK(cudaEventRecord(h->ev1, s));
+  return GATO_OK;
+}
+
+/* number of solves still active after the last enqueued pass (synchronises the stream).
+ * Non-zero only in loop modes 2/3 when a PCG-breakdown retry consumed a pass. */
+int gato_pending(gato_handle* h, void* stream, int32_t* pending) {
+  if (!h || !pending) return GATO_E_INVALID;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaStreamSynchronize(s));
+  unsigned int c[4];
+  CK(cudaMemcpy(c, h->P.counters, sizeof(c), cudaMemcpyDeviceToHost));
+  *pending = (int32_t)c[2];
+  return GATO_OK;
+}
+
+/* enqueue `passes` further SQP passes without re-initialising (loop modes 2/3 after retries) */
+int gato_resume(gato_handle* h, void* stream, int32_t passes) {
+  if (!h || !h->bound) return GATO_E_INVALID;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int it = 0; it < passes; ++it) {
+    int rc = enqueue_pass(h, s, 0);
+    if (rc != GATO_OK) return rc;
+  }
+  return GATO_OK;
+}
+
+int gato_shift_warm_start(gato_handle* h, void* stream) {
+  if (!h || !h->bound) return GATO_E_INVALID;
+  const SolveParams& P = h->P;
+  const size_t bytes = ((size_t)(P.N + 1) * h->ops.nx + (size_t)P.N * h->ops.nu) * sizeof(double);
+  if (bytes > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  }
+  k_shift<<<P.M, 128, bytes, static_cast<cudaStream_t>(stream)>>>(P.X, P.U, P.N, h->ops.nx, h->ops.nu);
+  CK(cudaGetLastError());
+  return GATO_OK;
+}
+
+int gato_scratch(gato_handle* h, const char* name, void** dev_ptr, int64_t* count) {
+  if (!h || !name || !dev_ptr) return GATO_E_INVALID;
+  for (const Scratch& s : h->scratch) {
+    if (strcmp(s.name, name) == 0) {
+      *dev_ptr = s.ptr;
+      if (count) *count = s.count;
+      return GATO_OK;
+    }
+  }
+  set_error(h, std::string("unknown scratch array ") + name);
+  return GATO_E_INVALID;
+}
+
+int gato_read_scratch(gato_handle* h, const char* name, void* host_dst, int64_t bytes) {
+  void* src = nullptr;
+  int64_t count = 0;
+  int rc = gato_scratch(h, name, &src, &count);
+  if (rc != GATO_OK) return rc;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(host_dst, src, (size_t)bytes, cudaMemcpyDeviceToHost));
+  return GATO_OK;
+}
+
+int64_t gato_launch_count(const gato_handle* h) {
+  if (!h) return 0;
+  unsigned int c[4] = {0, 0, 0, 0};
+  if (cudaMemcpy(c, h->P.counters, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return 3 + 6 * (int64_t)c[3];
+}
+
+int gato_loop_mode(const gato_handle* h) { return h ? h->loop_mode : 0; }
+
+int gato_last_solve_ms(gato_handle* h, float* ms) {
+  if (!h || !ms) return GATO_E_INVALID;
+  CK(cudaEventSynchronize(h->ev1));
+  CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
+  return GATO_OK;
+}
+
+const char* gato_last_error(const gato_handle* h) { return h ? h->error.c_str() : "null handle"; }
+
+void gato_destroy(gato_handle* h) {
+  if (!h) return;
+  destroy_graph(h);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  for (void* p : h->allocs) cudaFree(p);
+  delete h;
+}
+
+// ---- stateless operator entry points ----
+
+int gato_step_many(int32_t model_id, const double* model_params, int64_t rows, const double* X, const double* U,
+                   const double* F, double timestep, double* out, void* stream) {
+  ModelOps ops;
+  if (!select_ops(model_id, model_params, &ops) || rows < 0) return GATO_E_INVALID;
+  if (rows == 0) return GATO_OK;
+  ModelParams mp;
+  for (int i = 0; i < 8; ++i) mp.v[i] = model_params ? model_params[i] : 0.0;
+  cudaError_t err = ops.step_rows(mp, timestep, rows, X, U, F, out, static_cast<cudaStream_t>(stream));
+  return err == cudaSuccess ? GATO_OK : GATO_E_CUDA;
+}
+
+int gato_step_jacobians_many(int32_t model_id, const double* model_params, int64_t rows, const double* X,
+                             const double* U, const double* F, double timestep, double* A, double* B,
+                             void* stream) {
+  ModelOps ops;
+  if (!select_ops(model_id, model_params, &ops) || rows < 0) return GATO_E_INVALID;
+  if (rows == 0) return GATO_OK;
+  {
+    SolveParams tmp;
+    memset(&tmp, 0, sizeof(tmp));
+    tmp.N = 1;
+    if (ops.prepare(tmp) != cudaSuccess) return GATO_E_CUDA;
+  }
+  ModelParams mp;
+  for (int i = 0; i < 8; ++i) mp.v[i] = model_params ? model_params[i] : 0.0;
+  // operator mode: one "solve" whose N = rows, so row r is addressed as (b = 0, k = r); the
+  // defect output is off, so the (N+1)-th state row of the solve layout is never read.
+  RowView V{X, U, F, (int)rows, nullptr};
+  cudaError_t err = ops.linearize(V, mp, timestep, rows, A, B, nullptr, static_cast<cudaStream_t>(stream));
+  return err == cudaSuccess ? GATO_OK : GATO_E_CUDA;
+}
+
+int gato_pcg_batched(int32_t systems, int32_t nb, int32_t bd, const double* S_diag, const double* S_off,
+                     const double* gamma, const double* P_diag, const double* P_off, double tolerance,
+                     int32_t max_iterations, double* lam, int32_t* iterations, int32_t* converged, int32_t* status,
+                     double* residual, void* stream) {
+  if (systems < 1 || nb < 1 || bd < 1) return GATO_E_INVALID;
+  const int size = nb * bd;
+  const size_t bytes = ((size_t)6 * size + (size & 1)) * 8 + 64 * 16;
+  if (bytes > kMaxSmem) return GATO_E_INVALID;
+  const int cap = max_iterations > 0 ? max_iterations : 10 * size;
+  if (cudaFuncSetAttribute(k_pcg_explicit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return GATO_E_CUDA;
+  k_pcg_explicit<<<systems, 256, bytes, static_cast<cudaStream_t>(stream)>>>(
+      nb, bd, S_diag, S_off, gamma, P_diag, P_off, tolerance, cap, lam, iterations, converged, status, residual);
+  return cudaGetLastError() == cudaSuccess ? GATO_OK : GATO_E_CUDA;
+}
+
+}  // extern "C"

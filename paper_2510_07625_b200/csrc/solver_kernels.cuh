@@ -1,0 +1,984 @@
+// Kernels of one SQP pass, fp64, sm_100a.  One pass =
+//   k_hessinv     (Q+rho I)^-1, (QN+rho I)^-1, (R+rho I)^-1 per solve        qpform.py:296-311
+//   k_linearize_* A_k, B_k (exact RK4 Jacobians) and defects e_k per knot     qpform.py:181-183, dynamics.py:774-816
+//   k_schur       S (theta, phi), gamma, D^-1 per block row                   qpform.py:313-359
+//   k_pcg         PCG on S lam = gamma, step recovery, exit test              blocktri.py:123-173, qpform.py:375-397, sqp.py:253-272
+//   k_linesearch  merit of every (candidate, knot)                            sqp.py:132-166
+//   k_update      argmin / accept / X,U,rho update / trace / termination     sqp.py:189-195, 274-293
+// (paths relative to /root/reference/pkg/src/trajbatch/).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <climits>
+#include <cmath>
+
+#include "../../include/gato_b200.h"
+#include "models.cuh"
+
+namespace gato {
+
+// per-solve state words
+enum { SD_RHO = 0, SD_MERIT = 1, SD_VIOL = 2, SD_STEP_INF = 3, SD_WORDS = 4 };
+enum {
+  SI_ACTIVE = 0,
+  SI_IT = 1,
+  SI_RETRIES = 2,
+  SI_SKIP_LS = 3,
+  SI_PCG_ITS = 4,
+  SI_MERIT_VALID = 5,
+  SI_SCHUR_FAIL = 6,
+  SI_WORDS = 8
+};
+
+struct SolveParams {
+  int M, N, max_it, pcg_cap, C, regularize_r, retry_limit, pad0;
+  double h, pcg_tol, mu, rho_min, rho_max, rho_factor, step_tol, feas_tol;
+  ModelParams mp;
+  // caller buffers
+  const double *x_start, *goal, *Q, *R, *QN, *force, *rho_init;
+  double *X, *U, *trace;
+  int32_t* info;
+  // scratch
+  double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Dinv, *gamma, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
+  int32_t *si, *pcg_iters;
+  unsigned int* counters;  // [0] active count, [1] ticket, [2] pending solves, [3] passes run
+};
+
+// doubles per solve in hinv: [Qs^-1 | Qt^-1 | Rs^-1], padded to an even count (16-byte rows)
+__host__ __device__ constexpr int hinv_stride(int nx, int nu) { return (2 * nx * nx + nu * nu + 1) & ~1; }
+
+__device__ __forceinline__ double nanmax(double a, double b) { return (a > b || a != a) ? a : b; }
+
+__device__ __forceinline__ int tri_idx(int i, int j) { return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i; }
+
+// -----------------------------------------------------------------------------------------
+// Warp-cooperative SPD inverse: lower Cholesky, solve against I, symmetrise
+// (qpform.py:261-268; failure semantics of LAPACK dpotrf: pivot <= 0 or NaN -> 1-based index).
+// W: D*D row-major in shared memory (in: matrix, out: inverse), T: D*D scratch.
+// -----------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ int warp_spd_inverse(double* W, double* T, int lane) {
+  int fail = 0;
+  for (int j = 0; j < D; ++j) {
+    const double d = W[j * D + j];
+    if (!(d > 0.0)) {
+      fail = j + 1;
+      break;
+    }
+    const double r = sqrt(d);
+    __syncwarp();
+    if (lane == j) W[j * D + j] = r;
+    if (lane > j && lane < D) W[lane * D + j] = W[lane * D + j] / r;
+    __syncwarp();
+    if (lane > j && lane < D) {
+      const double lij = W[lane * D + j];
+      for (int k = j + 1; k <= lane; ++k) W[lane * D + k] = fma(-lij, W[k * D + j], W[lane * D + k]);
+    }
+    __syncwarp();
+  }
+  if (fail) return fail;
+  if (lane < D) {
+    double y[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double t = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) t = fma(-W[i * D + k], y[k], t);
+      y[i] = t / W[i * D + i];
+    }
+#pragma unroll
+    for (int i = D - 1; i >= 0; --i) {
+      double t = y[i];
+#pragma unroll
+      for (int k = i + 1; k < D; ++k) t = fma(-W[k * D + i], y[k], t);
+      y[i] = t / W[i * D + i];
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) T[i * D + lane] = y[i];
+  }
+  __syncwarp();
+  for (int idx = lane; idx < D * D; idx += 32) {
+    const int i = idx / D, j = idx % D;
+    W[idx] = 0.5 * (T[i * D + j] + T[j * D + i]);
+  }
+  __syncwarp();
+  return 0;
+}
+
+__device__ __forceinline__ void record_failure(const SolveParams& P, int b, int status, int knot, int block, int aux,
+                                               int retries) {
+  int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
+  info[GATO_INFO_STATUS] = status;
+  info[GATO_INFO_FAIL_ITER] = P.si[b * SI_WORDS + SI_IT];
+  info[GATO_INFO_FAIL_KNOT] = knot;
+  info[GATO_INFO_FAIL_BLOCK] = block;
+  info[GATO_INFO_FAIL_AUX] = aux;
+  info[GATO_INFO_RETRIES] = retries;
+  P.si[b * SI_WORDS + SI_ACTIVE] = 0;
+  P.si[b * SI_WORDS + SI_SKIP_LS] = 1;
+}
+
+// -----------------------------------------------------------------------------------------
+// k_hessinv: the three distinct damped Hessian blocks of one solve and their inverses
+// (linearize, qpform.py:177-179,193-196; memoised inverses, qpform.py:296-311).
+// hinv[b] = [ (Q+rho I)^-1 | (QN+rho I)^-1 | (R+rho I)^-1 ].  grid M, block 96.
+// -----------------------------------------------------------------------------------------
+template <int NX, int NU>
+__global__ void __launch_bounds__(96) k_hessinv(SolveParams P) {
+  const int b = blockIdx.x;
+  if (!P.si[b * SI_WORDS + SI_ACTIVE]) return;
+  __shared__ double W[3][NX * NX], T[3][NX * NX];
+  __shared__ int fails[3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double rho = P.sd[b * SD_WORDS + SD_RHO];
+  constexpr int HS = hinv_stride(NX, NU);
+  double* out = P.hinv + (size_t)b * HS;
+  if (warp < 2) {
+    const double* src = (warp == 0 ? P.Q : P.QN) + (size_t)b * NX * NX;
+    for (int idx = lane; idx < NX * NX; idx += 32) W[warp][idx] = src[idx] + ((idx / NX == idx % NX) ? rho : 0.0);
+    __syncwarp();
+    fails[warp] = warp_spd_inverse<NX>(W[warp], T[warp], lane);
+    for (int idx = lane; idx < NX * NX; idx += 32) out[warp * NX * NX + idx] = W[warp][idx];
+  } else {
+    const double* src = P.R + (size_t)b * NU * NU;
+    const double rr = P.regularize_r ? rho : 0.0;
+    for (int idx = lane; idx < NU * NU; idx += 32) W[2][idx] = src[idx] + ((idx / NU == idx % NU) ? rr : 0.0);
+    __syncwarp();
+    fails[2] = warp_spd_inverse<NU>(W[2], T[2], lane);
+    for (int idx = lane; idx < NU * NU; idx += 32) out[2 * NX * NX + idx] = W[2][idx];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // reporting order of form_schur: Q_0 .. Q_N first, then R_0 (qpform.py:305-311)
+    if (fails[0]) record_failure(P, b, GATO_STATUS_FACTORIZATION, 0, GATO_BLOCK_Q, fails[0], 0);
+    else if (fails[1]) record_failure(P, b, GATO_STATUS_FACTORIZATION, P.N, GATO_BLOCK_Q, fails[1], 0);
+    else if (fails[2]) record_failure(P, b, GATO_STATUS_FACTORIZATION, 0, GATO_BLOCK_R, fails[2], 0);
+  }
+}
+
+// -----------------------------------------------------------------------------------------
+// Row addressing shared by the solve (row r = solve b, knot k) and the stateless operator
+// entry points (M = 1, N = rows): X has N+1 rows per solve, U and F have N.
+// -----------------------------------------------------------------------------------------
+struct RowView {
+  const double *X, *U, *F;
+  int N;
+  const int32_t* si;  // null in operator mode
+};
+
+// -----------------------------------------------------------------------------------------
+// k_linearize_simple: analytic-Jacobian models, one thread per knot, the reference's own chain
+// rule through the four RK4 stages (dynamics.py:774-802).  e may be null (operator mode).
+// -----------------------------------------------------------------------------------------
+template <class Mdl>
+__global__ void k_linearize_simple(RowView V, ModelParams mp, double h, int64_t rows, double* __restrict__ A,
+                                   double* __restrict__ B, double* __restrict__ e) {
+  constexpr int NX = Mdl::NX, NU = Mdl::NU, NF = Mdl::NF;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t b = r / V.N, k = r % V.N;
+  if (V.si && !V.si[b * SI_WORDS + SI_ACTIVE]) return;
+  const double* xg = V.X + (b * (V.N + 1) + k) * NX;
+  double x[NX], u[NU], f[NF];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) x[i] = xg[i];
+#pragma unroll
+  for (int i = 0; i < NU; ++i) u[i] = V.U[r * NU + i];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) f[i] = V.F[r * NF + i];
+
+  double kk[NX], xs[NX], ksum[NX];
+  double gx[NX * NX], gu[NX * NU], sx[NX * NX], su[NX * NU], ax[NX * NX], au[NX * NU], tx[NX * NX], tu[NX * NU];
+  // stage 1
+  Mdl::deriv(mp, x, u, f, kk);
+  Mdl::jac(mp, x, u, f, sx, su);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) ax[i] = sx[i];
+#pragma unroll
+  for (int i = 0; i < NX * NU; ++i) au[i] = su[i];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) ksum[i] = kk[i];
+  for (int stage = 1; stage < 4; ++stage) {
+    const double lead = (stage == 3) ? h : 0.5 * h;
+    const double wgt = (stage == 3) ? 1.0 : 2.0;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) xs[i] = x[i] + lead * kk[i];
+    Mdl::jac(mp, xs, u, f, gx, gu);
+    // sx <- gx (I + lead sx) ; su <- gx (lead su) + gu
+    for (int i = 0; i < NX; ++i)
+      for (int j = 0; j < NX; ++j) {
+        double acc = 0.0;
+        for (int l = 0; l < NX; ++l) acc = fma(gx[i * NX + l], ((l == j) ? 1.0 : 0.0) + lead * sx[l * NX + j], acc);
+        tx[i * NX + j] = acc;
+      }
+    for (int i = 0; i < NX; ++i)
+      for (int j = 0; j < NU; ++j) {
+        double acc = 0.0;
+        for (int l = 0; l < NX; ++l) acc = fma(gx[i * NX + l], lead * su[l * NU + j], acc);
+        tu[i * NU + j] = acc + gu[i * NU + j];
+      }
+    for (int i = 0; i < NX * NX; ++i) {
+      sx[i] = tx[i];
+      ax[i] = ax[i] + wgt * tx[i];
+    }
+    for (int i = 0; i < NX * NU; ++i) {
+      su[i] = tu[i];
+      au[i] = au[i] + wgt * tu[i];
+    }
+    Mdl::deriv(mp, xs, u, f, kk);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) ksum[i] = ksum[i] + wgt * kk[i];
+  }
+  double* Ag = A + r * NX * NX;
+  double* Bg = B + r * NX * NU;
+  for (int i = 0; i < NX; ++i)
+    for (int j = 0; j < NX; ++j) Ag[i * NX + j] = ((i == j) ? 1.0 : 0.0) + (h / 6.0) * ax[i * NX + j];
+  for (int i = 0; i < NX * NU; ++i) Bg[i] = (h / 6.0) * au[i];
+  if (e) {
+    const double* xn = xg + NX;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) e[r * NX + i] = (x[i] + (h / 6.0) * ksum[i]) - xn[i];
+  }
+}
+
+// -----------------------------------------------------------------------------------------
+// k_linearize_iiwa: a group of G lanes per knot.  Lane 0 of the group runs the four primal
+// RK4 stages and leaves the per-stage link data in shared memory; then every lane carries one
+// tangent direction (14 state + 7 control columns) through the four stages: column d of
+// [A | B] is the exact derivative of the RK4 map along that direction -- the same chain rule
+// as dynamics.py:774-802, evaluated as Jacobian-vector products so no n x n x n product and
+// no cross-lane traffic is needed.
+// -----------------------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(128) k_linearize_iiwa(RowView V, double h, int64_t rows, double* __restrict__ A,
+                                                        double* __restrict__ B, double* __restrict__ e) {
+  constexpr int NX = 14, NU = 7, NF = 3;
+  extern __shared__ double lin_smem[];
+  const int gid = threadIdx.x / G, gl = threadIdx.x % G;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / G) + gid;
+  bool valid = r < rows;
+  int64_t b = 0, k = 0;
+  if (valid) {
+    b = r / V.N;
+    k = r % V.N;
+    if (V.si && !V.si[b * SI_WORDS + SI_ACTIVE]) valid = false;
+  }
+  iiwa::Stage* st = reinterpret_cast<iiwa::Stage*>(lin_smem) + gid * 4;
+  double f[NF] = {0, 0, 0};
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NF; ++i) f[i] = V.F[r * NF + i];
+  }
+  if (valid && gl == 0) {
+    const double* xg = V.X + (b * (V.N + 1) + k) * NX;
+    double x[NX], u[NU], kk[NX], xs[NX], ksum[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) x[i] = xg[i];
+#pragma unroll
+    for (int i = 0; i < NU; ++i) u[i] = V.U[r * NU + i];
+    iiwa::forward_dynamics<true>(x, u, f, kk, &st[0]);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      ksum[i] = kk[i];
+      xs[i] = x[i] + 0.5 * h * kk[i];
+    }
+    iiwa::forward_dynamics<true>(xs, u, f, kk, &st[1]);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      ksum[i] = ksum[i] + 2.0 * kk[i];
+      xs[i] = x[i] + 0.5 * h * kk[i];
+    }
+    iiwa::forward_dynamics<true>(xs, u, f, kk, &st[2]);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      ksum[i] = ksum[i] + 2.0 * kk[i];
+      xs[i] = x[i] + h * kk[i];
+    }
+    iiwa::forward_dynamics<true>(xs, u, f, kk, &st[3]);
+    if (e) {
+      const double* xn = xg + NX;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) e[r * NX + i] = (x[i] + (h / 6.0) * (ksum[i] + kk[i])) - xn[i];
+    }
+  }
+  __syncwarp();
+  if (!valid) return;
+  for (int d = gl; d < NX + NU; d += G) {
+    const int du = (d >= NX) ? d - NX : -1;
+    double dx[NX], dk[NX], acc[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) dx[i] = (i == d) ? 1.0 : 0.0;
+    iiwa::tangent(&st[0], f, dx, du, dk);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      acc[i] = dk[i];
+      dx[i] = ((i == d) ? 1.0 : 0.0) + 0.5 * h * dk[i];
+    }
+    iiwa::tangent(&st[1], f, dx, du, dk);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      acc[i] = acc[i] + 2.0 * dk[i];
+      dx[i] = ((i == d) ? 1.0 : 0.0) + 0.5 * h * dk[i];
+    }
+    iiwa::tangent(&st[2], f, dx, du, dk);
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      acc[i] = acc[i] + 2.0 * dk[i];
+      dx[i] = ((i == d) ? 1.0 : 0.0) + h * dk[i];
+    }
+    iiwa::tangent(&st[3], f, dx, du, dk);
+    if (d < NX) {
+      double* Ag = A + r * NX * NX;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) Ag[i * NX + d] = ((i == d) ? 1.0 : 0.0) + (h / 6.0) * (acc[i] + dk[i]);
+    } else {
+      double* Bg = B + r * NX * NU;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) Bg[i * NU + du] = (h / 6.0) * (acc[i] + dk[i]);
+    }
+  }
+}
+
+// k_step_rows: out[r] = RK4 step of row r (dynamics.py:805-816), one thread per row.
+template <class Mdl>
+__global__ void k_step_rows(ModelParams mp, double h, int64_t rows, const double* __restrict__ X,
+                            const double* __restrict__ U, const double* __restrict__ F, double* __restrict__ out) {
+  constexpr int NX = Mdl::NX, NU = Mdl::NU, NF = Mdl::NF;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double x[NX], u[NU], f[NF], o[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) x[i] = X[r * NX + i];
+#pragma unroll
+  for (int i = 0; i < NU; ++i) u[i] = U[r * NU + i];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) f[i] = F[r * NF + i];
+  rk4_step<Mdl>(mp, x, u, f, h, o);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) out[r * NX + i] = o[i];
+}
+
+// -----------------------------------------------------------------------------------------
+// k_schur: one warp per block row k of one solve (form_schur qpform.py:290-339 and the
+// diagonal part of form_preconditioner qpform.py:342-353):
+//   k = 0 : S_00 = Q_0^-1, gamma_0 = Q_0^-1 q_0 + (x_s - x_0)
+//   k > 0 : theta = A Q^-1 A^T + B R^-1 B^T + Q_k^-1, phi = -A Q^-1, gamma_k = zeta + e
+//   D_k^-1 = spd_inverse(S_kk).
+// The stair preconditioner's off-diagonal blocks -D_{k+1}^-1 phi_k D_k^-1 (qpform.py:355-356)
+// are never formed: k_pcg applies Phi^-1 in factored form, which needs no neighbour's D^-1
+// here and therefore no grid-wide synchronisation.
+// -----------------------------------------------------------------------------------------
+template <int NX, int NU>
+struct SchurSmem {
+  double A[NX * NX], B[NX * NU], AQ[NX * NX], BR[NX * NU], W[NX * NX], T[NX * NX];
+  double qk[NX], qj[NX], rj[NU], dxk[NX], dxj[NX];
+};
+
+template <int NX, int NU, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_schur(SolveParams P) {
+  extern __shared__ double schur_smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wg = (int64_t)blockIdx.x * WARPS + warp;
+  const int nb = P.N + 1;
+  if (wg >= (int64_t)P.M * nb) return;
+  const int b = (int)(wg / nb), k = (int)(wg % nb);
+  if (!P.si[b * SI_WORDS + SI_ACTIVE]) return;
+  SchurSmem<NX, NU>& S = reinterpret_cast<SchurSmem<NX, NU>*>(schur_smem_raw)[warp];
+  constexpr int HS = hinv_stride(NX, NU);
+  constexpr int TRI = NX * (NX + 1) / 2;
+  const double* Qi = P.hinv + (size_t)b * HS;
+  const double* Qti = Qi + NX * NX;
+  const double* Ri = Qi + 2 * NX * NX;
+  const double* Xb = P.X + (size_t)b * nb * NX;
+  const double* Gb = P.goal + (size_t)b * nb * NX;
+  const double* Qw = P.Q + (size_t)b * NX * NX;
+  const double* QNw = P.QN + (size_t)b * NX * NX;
+  const double* Rw = P.R + (size_t)b * NU * NU;
+  double* grad = P.grad + ((size_t)b * nb + k) * (NX + NU);
+
+  // gradients with the undamped weights (qpform.py:185-186,195)
+  if (lane < NX) {
+    S.dxk[lane] = Xb[k * NX + lane] - Gb[k * NX + lane];
+    if (k > 0) S.dxj[lane] = Xb[(k - 1) * NX + lane] - Gb[(k - 1) * NX + lane];
+  }
+  __syncwarp();
+  if (lane < NX) {
+    const double* Wt = (k < P.N) ? Qw : QNw;
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) acc = fma(Wt[lane * NX + j], S.dxk[j], acc);
+    S.qk[lane] = acc;
+    grad[lane] = acc;
+    if (k > 0) {
+      double a2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) a2 = fma(Qw[lane * NX + j], S.dxj[j], a2);
+      S.qj[lane] = a2;
+    }
+  }
+  if (lane < NU) {
+    if (k < P.N) {
+      const double* uk = P.U + ((size_t)b * P.N + k) * NU;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NU; ++j) acc = fma(Rw[lane * NU + j], uk[j], acc);
+      grad[NX + lane] = acc;
+    }
+    if (k > 0) {
+      const double* uj = P.U + ((size_t)b * P.N + k - 1) * NU;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NU; ++j) acc = fma(Rw[lane * NU + j], uj[j], acc);
+      S.rj[lane] = acc;
+    }
+  }
+  __syncwarp();
+
+  double* Sd = P.Sdiag + ((size_t)b * nb + k) * NX * NX;
+  double* gam = P.gamma + ((size_t)b * nb + k) * NX;
+  if (k == 0) {
+    for (int idx = lane; idx < NX * NX; idx += 32) {
+      const double v = Qi[idx];
+      S.W[idx] = v;
+      Sd[idx] = v;
+    }
+    if (lane < NX) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) acc = fma(Qi[lane * NX + j], S.qk[j], acc);
+      gam[lane] = acc + (P.x_start[(size_t)b * NX + lane] - Xb[lane]);
+    }
+  } else {
+    const int j = k - 1;
+    const double* Ag = P.A + ((size_t)b * P.N + j) * NX * NX;
+    const double* Bg = P.B + ((size_t)b * P.N + j) * NX * NU;
+    for (int idx = lane; idx < NX * NX; idx += 32) S.A[idx] = Ag[idx];
+    for (int idx = lane; idx < NX * NU; idx += 32) S.B[idx] = Bg[idx];
+    __syncwarp();
+    for (int idx = lane; idx < NX * NX; idx += 32) {
+      const int r = idx / NX, c = idx % NX;
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < NX; ++l) acc = fma(S.A[r * NX + l], Qi[l * NX + c], acc);
+      S.AQ[idx] = acc;
+    }
+    for (int idx = lane; idx < NX * NU; idx += 32) {
+      const int r = idx / NU, c = idx % NU;
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < NU; ++l) acc = fma(S.B[r * NU + l], Ri[l * NU + c], acc);
+      S.BR[idx] = acc;
+    }
+    __syncwarp();
+    const double* Qk = (k < P.N) ? Qi : Qti;
+    double* So = P.Soff + ((size_t)b * P.N + j) * NX * NX;
+    for (int idx = lane; idx < NX * NX; idx += 32) {
+      const int r = idx / NX, c = idx % NX;
+      double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+      for (int l = 0; l < NX; ++l) t1 = fma(S.AQ[r * NX + l], S.A[c * NX + l], t1);
+#pragma unroll
+      for (int l = 0; l < NU; ++l) t2 = fma(S.BR[r * NU + l], S.B[c * NU + l], t2);
+      const double th = (t1 + t2) + Qk[idx];
+      S.W[idx] = th;
+      Sd[idx] = th;
+      So[idx] = -S.AQ[idx];
+    }
+    if (lane < NX) {
+      double z1 = 0.0, z2 = 0.0, z3 = 0.0;
+#pragma unroll
+      for (int l = 0; l < NX; ++l) z1 = fma(S.AQ[lane * NX + l], S.qj[l], z1);
+#pragma unroll
+      for (int l = 0; l < NU; ++l) z2 = fma(S.BR[lane * NU + l], S.rj[l], z2);
+#pragma unroll
+      for (int l = 0; l < NX; ++l) z3 = fma(Qk[lane * NX + l], S.qk[l], z3);
+      const double zeta = (-z1 - z2) + z3;
+      gam[lane] = zeta + P.e[((size_t)b * P.N + j) * NX + lane];
+    }
+  }
+  __syncwarp();
+  const int fail = warp_spd_inverse<NX>(S.W, S.T, lane);
+  if (fail) {
+    if (lane == 0) atomicMin(&P.si[b * SI_WORDS + SI_SCHUR_FAIL], k * 64 + fail);
+    return;
+  }
+  double* Dk = P.Dinv + ((size_t)b * nb + k) * TRI;
+  for (int idx = lane; idx < NX * NX; idx += 32) {
+    const int r = idx / NX, c = idx % NX;
+    if (c <= r) Dk[r * (r + 1) / 2 + c] = S.W[idx];
+  }
+}
+
+// -----------------------------------------------------------------------------------------
+// k_pcg: one CTA per solve.  Thread (k, i) owns rows i and i + NX/2 of block row k.
+//   - its two rows of the diagonal block S_kk live in registers for the whole solve,
+//   - the sub-diagonal blocks phi_k and the packed D_k^-1 live in shared memory (or stay in
+//     global memory when the horizon is too long for 227 KB: SMEM_MATS = false),
+//   - Phi^-1 r is applied in factored form  z_k = D_k^-1 (r_k - phi_{k-1} w_{k-1} - phi_k^T w_{k+1}),
+//     w = D^-1 r, algebraically identical to the explicit stair blocks of qpform.py:355-356,
+//   - dot products: fixed xor-shuffle tree inside a warp, fixed-order sum over warps
+//     (bitwise reproducible, independent of batch position),
+//   - stop test on the recurrence residual ||r||_2 (the reference recomputes ||S lam - gamma||,
+//     blocktri.py:165; SURVEY.md 3.3 measured identical iteration counts in fp64).
+// Then the primal step (qpform.py:375-397), ||dZ||_inf, the violation of the current iterate
+// (sqp.py:254) and the tolerance exit (sqp.py:256-272).
+// -----------------------------------------------------------------------------------------
+template <int NX>
+__device__ __forceinline__ double dot_row(const double* __restrict__ row, const double* __restrict__ v) {
+  double acc = 0.0;
+  if constexpr (NX % 2 == 0) {
+    const double2* r2 = reinterpret_cast<const double2*>(row);
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+#pragma unroll
+    for (int j = 0; j < NX / 2; ++j) {
+      const double2 a = r2[j], c = v2[j];
+      acc = fma(a.x, c.x, acc);
+      acc = fma(a.y, c.y, acc);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NX; ++j) acc = fma(row[j], v[j], acc);
+  }
+  return acc;
+}
+
+struct BlockReducer {
+  double2* red;  // [2][32]
+  int flip;
+  int nwarps;
+  // sum of (a, b) over the CTA, same value in every thread
+  __device__ __forceinline__ double2 sum2(double a, double b) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    double2* buf = red + flip * 32;
+    flip ^= 1;
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = make_double2(a, b);
+    __syncthreads();
+    double sa = 0.0, sb = 0.0;
+    for (int w = 0; w < nwarps; ++w) {
+      const double2 v = buf[w];
+      sa += v.x;
+      sb += v.y;
+    }
+    return make_double2(sa, sb);
+  }
+  __device__ __forceinline__ double max1(double a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = nanmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    double2* buf = red + flip * 32;
+    flip ^= 1;
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = make_double2(a, 0.0);
+    __syncthreads();
+    double m = buf[0].x;
+    for (int w = 1; w < nwarps; ++w) m = nanmax(m, buf[w].x);
+    return m;
+  }
+};
+
+template <int NX, int NU, bool SMEM_MATS, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_pcg(SolveParams P) {
+  constexpr bool SD_REGS = (MAXT <= 512);  // 128 registers per thread available
+  constexpr int HN = NX / 2, TRI = NX * (NX + 1) / 2, BS = NX * NX;
+  constexpr int HS = hinv_stride(NX, NU);
+  const int b = blockIdx.x;
+  int32_t* si = P.si + b * SI_WORDS;
+  if (!si[SI_ACTIVE]) return;
+  const int N = P.N, nb = N + 1;
+  const int t = threadIdx.x;
+  if (si[SI_SCHUR_FAIL] != INT_MAX) {
+    if (t == 0) {
+      const int key = si[SI_SCHUR_FAIL];
+      si[SI_SCHUR_FAIL] = INT_MAX;
+      record_failure(P, b, GATO_STATUS_FACTORIZATION, key / 64, GATO_BLOCK_S, key % 64, 0);
+    }
+    return;
+  }
+  extern __shared__ __align__(16) double pcg_smem[];
+  const int vlen = nb * NX;
+  const int vpad = (vlen + 1) & ~1;
+  double* vp = pcg_smem;       // search direction p
+  double* vr = vp + vpad;      // residual r, later r - t
+  double* vw = vr + vpad;      // w = D^-1 r
+  double2* red = reinterpret_cast<double2*>(vw + vpad);
+  double* mats = reinterpret_cast<double*>(red + 64);
+  const double* So;
+  const double* Di;
+  if constexpr (SMEM_MATS) {
+    double* sSo = mats;
+    double* sDi = mats + (size_t)N * BS;
+    const double2* gSo = reinterpret_cast<const double2*>(P.Soff + (size_t)b * N * BS);
+    for (int idx = t; idx < N * BS / 2; idx += blockDim.x) reinterpret_cast<double2*>(sSo)[idx] = gSo[idx];
+    const double* gDi = P.Dinv + (size_t)b * nb * TRI;
+    for (int idx = t; idx < nb * TRI; idx += blockDim.x) sDi[idx] = gDi[idx];
+    So = sSo;
+    Di = sDi;
+  } else {
+    So = P.Soff + (size_t)b * N * BS;
+    Di = P.Dinv + (size_t)b * nb * TRI;
+  }
+  const bool valid = t < nb * HN;
+  const int k = valid ? t / HN : 0;
+  const int i0 = valid ? t % HN : 0, i1 = i0 + HN;
+  BlockReducer R{red, 0, (int)((blockDim.x + 31) >> 5)};
+
+  const double* Sdk = P.Sdiag + ((size_t)b * nb + k) * BS;
+  double sd0[SD_REGS ? NX : 1], sd1[SD_REGS ? NX : 1];
+  if constexpr (SD_REGS) {
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      sd0[j] = valid ? Sdk[i0 * NX + j] : 0.0;
+      sd1[j] = valid ? Sdk[i1 * NX + j] : 0.0;
+    }
+  }
+  const double* gam = P.gamma + (size_t)b * vlen;
+  double r0 = valid ? gam[k * NX + i0] : 0.0, r1 = valid ? gam[k * NX + i1] : 0.0;
+  double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
+
+  // violation of the current iterate: |x_s - x_0|_1 + sum |e|_1  (sqp.py:111-115)
+  double viol_part = 0.0;
+  if (valid) {
+    if (k < N) {
+      const double* eb = P.e + ((size_t)b * N + k) * NX;
+      viol_part = fabs(eb[i0]) + fabs(eb[i1]);
+    }
+    if (k == 0) {
+      const double* xs = P.x_start + (size_t)b * NX;
+      const double* x0 = P.X + (size_t)b * nb * NX;
+      viol_part += fabs(xs[i0] - x0[i0]) + fabs(xs[i1] - x0[i1]);
+    }
+  }
+
+  // off-diagonal product rows (k,i0),(k,i1) of  phi_{k-1} v_{k-1} + phi_k^T v_{k+1}
+  auto offmv = [&](const double* v, double& y0, double& y1) {
+    y0 = 0.0;
+    y1 = 0.0;
+    if (k > 0) {
+      const double* O = So + (size_t)(k - 1) * BS;
+      const double* vm = v + (k - 1) * NX;
+      y0 = dot_row<NX>(O + i0 * NX, vm);
+      y1 = dot_row<NX>(O + i1 * NX, vm);
+    }
+    if (k < N) {
+      const double* O = So + (size_t)k * BS;
+      const double* vn = v + (k + 1) * NX;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        s0 = fma(O[j * NX + i0], vn[j], s0);
+        s1 = fma(O[j * NX + i1], vn[j], s1);
+      }
+      y0 += s0;
+      y1 += s1;
+    }
+  };
+  auto dinv_apply = [&](const double* v, double& y0, double& y1) {
+    const double* D = Di + (size_t)k * TRI;
+    const double* vk = v + k * NX;
+    const int base0 = i0 * (i0 + 1) / 2, base1 = i1 * (i1 + 1) / 2;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      const int tj = j * (j + 1) / 2;
+      const double vj = vk[j];
+      a0 = fma(D[(j <= i0) ? base0 + j : tj + i0], vj, a0);
+      a1 = fma(D[(j <= i1) ? base1 + j : tj + i1], vj, a1);
+    }
+    y0 = a0;
+    y1 = a1;
+  };
+  // z = Phi^-1 r for the current (r0, r1); uses vr, vw; result thread-private
+  auto precondition = [&](double& z0, double& z1) {
+    if (valid) {
+      vr[k * NX + i0] = r0;
+      vr[k * NX + i1] = r1;
+    }
+    __syncthreads();
+    double w0 = 0.0, w1 = 0.0;
+    if (valid) {
+      dinv_apply(vr, w0, w1);
+      vw[k * NX + i0] = w0;
+      vw[k * NX + i1] = w1;
+    }
+    __syncthreads();
+    double t0 = 0.0, t1 = 0.0;
+    if (valid) {
+      offmv(vw, t0, t1);  // every read of vr (dinv_apply above) precedes the barrier just passed
+      vr[k * NX + i0] = r0 - t0;
+      vr[k * NX + i1] = r1 - t1;
+    }
+    __syncthreads();
+    if (valid) dinv_apply(vr, z0, z1);
+    else z0 = z1 = 0.0;
+  };
+
+  int its = 0, breakdown = 0;
+  bool nan_curv = false;
+  double2 s = R.sum2(r0 * r0 + r1 * r1, viol_part);
+  double res = sqrt(s.x);
+  const double viol = s.y;
+  if (!(res <= P.pcg_tol)) {
+    double z0, z1;
+    precondition(z0, z1);
+    p0 = z0;
+    p1 = z1;
+    double rz = R.sum2(r0 * z0 + r1 * z1, 0.0).x;
+    const int cap = P.pcg_cap;
+    for (int it = 1; it <= cap; ++it) {
+      if (valid) {
+        vp[k * NX + i0] = p0;
+        vp[k * NX + i1] = p1;
+      }
+      __syncthreads();
+      double q0 = 0.0, q1 = 0.0;
+      if (valid) {
+        const double* vk = vp + k * NX;
+        double a0 = 0.0, a1 = 0.0;
+        if constexpr (SD_REGS) {
+#pragma unroll
+          for (int j = 0; j < NX; ++j) {
+            a0 = fma(sd0[j], vk[j], a0);
+            a1 = fma(sd1[j], vk[j], a1);
+          }
+        } else {
+          a0 = dot_row<NX>(Sdk + i0 * NX, vk);
+          a1 = dot_row<NX>(Sdk + i1 * NX, vk);
+        }
+        double o0, o1;
+        offmv(vp, o0, o1);
+        q0 = a0 + o0;
+        q1 = a1 + o1;
+      }
+      const double curv = R.sum2(p0 * q0 + p1 * q1, 0.0).x;
+      if (curv <= 0.0) {  // blocktri.py:158-161
+        breakdown = it;
+        break;
+      }
+      if (curv != curv) {  // NaN never satisfies a comparison: the reference runs to the cap
+        nan_curv = true;
+        its = cap;
+        break;
+      }
+      const double a = rz / curv;
+      l0 = l0 + a * p0;
+      l1 = l1 + a * p1;
+      r0 = r0 - a * q0;
+      r1 = r1 - a * q1;
+      double z0n, z1n;
+      precondition(z0n, z1n);
+      const double2 rr = R.sum2(r0 * z0n + r1 * z1n, r0 * r0 + r1 * r1);
+      res = sqrt(rr.y);
+      its = it;
+      if (res <= P.pcg_tol) break;
+      const double beta = rr.x / rz;
+      p0 = z0n + beta * p0;
+      p1 = z1n + beta * p1;
+      rz = rr.x;
+    }
+  }
+  if (nan_curv) l0 = l1 = nan("");
+
+  if (breakdown) {
+    if (t == 0) {
+      const int retries = si[SI_RETRIES] + 1;
+      si[SI_RETRIES] = retries;
+      if (retries > P.retry_limit) {  // sqp.py:242-247
+        record_failure(P, b, GATO_STATUS_PCG_BREAKDOWN, -1, 0, breakdown, retries);
+      } else {  // sqp.py:248
+        P.sd[b * SD_WORDS + SD_RHO] = fmin(P.sd[b * SD_WORDS + SD_RHO] * P.rho_factor, P.rho_max);
+        si[SI_SKIP_LS] = 1;
+      }
+    }
+    return;
+  }
+
+  // ---- recover_step (qpform.py:375-397) ----
+  __syncthreads();
+  double* vl = vp;  // lambda
+  double* vg = vr;  // grad_x
+  double* vu = vw;  // grad_u  [N][NU]
+  if (valid) {
+    vl[k * NX + i0] = l0;
+    vl[k * NX + i1] = l1;
+    P.lam[(size_t)b * vlen + k * NX + i0] = l0;
+    P.lam[(size_t)b * vlen + k * NX + i1] = l1;
+  }
+  __syncthreads();
+  const double* hinv = P.hinv + (size_t)b * HS;
+  if (valid) {
+    const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
+    double g0 = g[i0] - l0, g1 = g[i1] - l1;
+    if (k < N) {
+      const double* Ak = P.A + ((size_t)b * N + k) * BS;
+      const double* ln = vl + (k + 1) * NX;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        s0 = fma(Ak[j * NX + i0], ln[j], s0);
+        s1 = fma(Ak[j * NX + i1], ln[j], s1);
+      }
+      g0 += s0;
+      g1 += s1;
+      const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
+      for (int ju = i0; ju < NU; ju += HN) {
+        double su = 0.0;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) su = fma(Bk[j * NU + ju], ln[j], su);
+        vu[k * NU + ju] = g[NX + ju] + su;
+      }
+    }
+    vg[k * NX + i0] = g0;
+    vg[k * NX + i1] = g1;
+  }
+  __syncthreads();
+  double step_part = 0.0;
+  if (valid) {
+    const double* Qk = (k < N) ? hinv : hinv + BS;
+    const double* gk = vg + k * NX;
+    const double d0 = -dot_row<NX>(Qk + i0 * NX, gk);
+    const double d1 = -dot_row<NX>(Qk + i1 * NX, gk);
+    double* dX = P.dX + ((size_t)b * nb + k) * NX;
+    dX[i0] = d0;
+    dX[i1] = d1;
+    step_part = nanmax(fabs(d0), fabs(d1));
+    if (k < N) {
+      const double* Ri = hinv + 2 * BS;
+      const double* gu = vu + k * NU;
+      double* dU = P.dU + ((size_t)b * N + k) * NU;
+      for (int ju = i0; ju < NU; ju += HN) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
+        dU[ju] = -acc;
+        step_part = nanmax(step_part, fabs(acc));
+      }
+    }
+  }
+  const double step_inf = R.max1(step_part);
+  if (t == 0) {
+    si[SI_RETRIES] = 0;
+    si[SI_PCG_ITS] = its;
+    P.sd[b * SD_WORDS + SD_STEP_INF] = step_inf;
+    P.sd[b * SD_WORDS + SD_VIOL] = viol;
+    const int it = si[SI_IT];
+    P.pcg_iters[(size_t)b * P.max_it + it] = its;
+    const bool tol_mode = P.step_tol == P.step_tol;  // NaN => None
+    if (tol_mode && step_inf <= P.step_tol && viol <= P.feas_tol) {  // sqp.py:256-272
+      double* tr = P.trace + ((size_t)b * P.max_it + it) * GATO_TRACE_WORDS;
+      tr[GATO_TRACE_MERIT] = P.sd[b * SD_WORDS + SD_MERIT];
+      tr[GATO_TRACE_CONSTRAINT_L1] = viol;
+      tr[GATO_TRACE_ALPHA] = nan("");
+      tr[GATO_TRACE_RHO] = P.sd[b * SD_WORDS + SD_RHO];
+      tr[GATO_TRACE_PCG_ITERATIONS] = (double)its;
+      tr[GATO_TRACE_ACCEPTED] = 0.0;
+      tr[GATO_TRACE_STEP_INF_NORM] = step_inf;
+      tr[GATO_TRACE_ITERATION] = (double)it;
+      int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
+      info[GATO_INFO_N_RECORDS] = it + 1;
+      info[GATO_INFO_CONVERGED] = 1;
+      si[SI_ACTIVE] = 0;
+      si[SI_SKIP_LS] = 1;
+    } else {
+      si[SI_SKIP_LS] = 0;
+    }
+  }
+}
+
+// -----------------------------------------------------------------------------------------
+// k_linesearch: merit of every candidate (sqp.py:132-166).  grid (C, M), one thread per stage
+// knot: candidate point (X + a dX, U + a dU), one RK4 prediction, |defect|_1, quadratic cost
+// with the undamped weights; fixed-tree reduction over knots.  Non-finite candidates -> +inf.
+// `init` = 1 evaluates only candidate 0 at alpha = 0 (the initial merit, sqp.py:229).
+// -----------------------------------------------------------------------------------------
+template <class Mdl>
+__global__ void __launch_bounds__(128) k_linesearch(SolveParams P, int init) {
+  constexpr int NX = Mdl::NX, NU = Mdl::NU, NF = Mdl::NF;
+  const int c = blockIdx.x, b = blockIdx.y;
+  const int32_t* si = P.si + b * SI_WORDS;
+  if (!si[SI_ACTIVE]) return;
+  if (!init && si[SI_SKIP_LS]) return;
+  __shared__ double2 red[2 * 32];
+  __shared__ int bad_flag;
+  if (threadIdx.x == 0) bad_flag = 0;
+  __syncthreads();
+  const int N = P.N, nb = N + 1;
+  const double alpha = init ? 0.0 : P.alphas[c];
+  double cost = 0.0, viol = 0.0;
+  int bad = 0;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const double* Xk = P.X + ((size_t)b * nb + k) * NX;
+    const double* dXk = P.dX + ((size_t)b * nb + k) * NX;
+    const double* Uk = P.U + ((size_t)b * N + k) * NU;
+    const double* dUk = P.dU + ((size_t)b * N + k) * NU;
+    const double* Gk = P.goal + ((size_t)b * nb + k) * NX;
+    double x[NX], xn[NX], u[NU], f[NF], pred[NX], dx[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      x[i] = Xk[i] + alpha * dXk[i];
+      xn[i] = Xk[NX + i] + alpha * dXk[NX + i];
+      bad |= !isfinite(x[i]);
+      if (k == N - 1) bad |= !isfinite(xn[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      u[i] = Uk[i] + alpha * dUk[i];
+      bad |= !isfinite(u[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NF; ++i) f[i] = P.force[((size_t)b * N + k) * NF + i];
+    rk4_step<Mdl>(P.mp, x, u, f, P.h, pred);
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) v += fabs(pred[i] - xn[i]);
+    if (k == 0) {
+      const double* xs = P.x_start + (size_t)b * NX;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) v += fabs(xs[i] - x[i]);
+    }
+    viol += v;
+    const double* Qw = P.Q + (size_t)b * NX * NX;
+    const double* Rw = P.R + (size_t)b * NU * NU;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) dx[i] = x[i] - Gk[i];
+    double cq = 0.0;
+    for (int i = 0; i < NX; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) acc = fma(Qw[i * NX + j], dx[j], acc);
+      cq = fma(dx[i], acc, cq);
+    }
+    double cr = 0.0;
+    for (int i = 0; i < NU; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NU; ++j) acc = fma(Rw[i * NU + j], u[j], acc);
+      cr = fma(u[i], acc, cr);
+    }
+    double cn = 0.0;
+    if (k == N - 1) {
+      const double* QNw = P.QN + (size_t)b * NX * NX;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) dx[i] = xn[i] - Gk[NX + i];
+      for (int i = 0; i < NX; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) acc = fma(QNw[i * NX + j], dx[j], acc);
+        cn = fma(dx[i], acc, cn);
+      }
+    }
+    cost += 0.5 * cq + 0.5 * cr + 0.5 * cn;
+  }
+  if (bad) atomicOr(&bad_flag, 1);
+  BlockReducer R{red, 0, (int)((blockDim.x + 31) >> 5)};
+  const double2 s = R.sum2(cost, viol);
+  if (threadIdx.x == 0) {
+    double value = s.x + P.mu * s.y;
+    if (bad_flag || !isfinite(value)) value = INFINITY;
+    P.merits[(size_t)b * P.C + c] = value;
+    P.viols[(size_t)b * P.C + c] = s.y;
+  }
+}
+
+}  // namespace gato

@@ -1,0 +1,317 @@
+"""Device engine: one gato handle + its device/pinned buffers for a fixed
+(model, M, N, timestep, settings) configuration on one GPU.
+
+torch is used for device memory, pinned host staging and streams only; every kernel runs
+behind the C ABI (include/gato_b200.h).  The array-level API here is what an MPC loop uses
+(buffers stay resident between control steps); `batch.batch_solve`
+is the reference-typed wrapper on top of it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import BackendUnavailableError
+from .models import device_model
+from .settings import SolverSettings
+
+# inputs of one batch, in the order they are staged host->device
+INPUT_FIELDS = ("x_start", "goal", "Q", "R", "QN", "force", "rho_init", "X", "U")
+
+
+@dataclass
+class PackedBatch:
+    """Host arrays of one homogeneous batch (C-contiguous float64).
+
+    x_start (M, n) | goal (M, N+1, n) | Q (M, n, n) | R (M, m, m) | QN (M, n, n) |
+    force (M, N, fdim) | rho_init (M,) | X (M, N+1, n) | U (M, N, m)
+    """
+
+    x_start: np.ndarray
+    goal: np.ndarray
+    Q: np.ndarray
+    R: np.ndarray
+    QN: np.ndarray
+    force: np.ndarray
+    rho_init: np.ndarray
+    X: np.ndarray
+    U: np.ndarray
+
+    @property
+    def size(self) -> int:
+        return self.x_start.shape[0]
+
+    def slice(self, lo: int, hi: int) -> "PackedBatch":
+        return PackedBatch(*(getattr(self, f)[lo:hi] for f in INPUT_FIELDS))
+
+    def nbytes(self) -> int:
+        return sum(getattr(self, f).nbytes for f in INPUT_FIELDS)
+
+
+@dataclass
+class PackedResult:
+    X: np.ndarray         # (M, N+1, n)
+    U: np.ndarray         # (M, N, m)
+    trace: np.ndarray     # (M, max_it, TRACE_WORDS)
+    info: np.ndarray      # (M, INFO_WORDS) int32
+    device_ms: float
+
+    def nbytes(self) -> int:
+        return self.X.nbytes + self.U.nbytes + self.trace.nbytes + self.info.nbytes
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as exc:  # pragma: no cover
+        raise BackendUnavailableError("torch is required for device buffers") from exc
+    if not torch.cuda.is_available():
+        raise BackendUnavailableError(
+            "no CUDA device visible: the batched SQP solve runs only on the GPU (no CPU fallback)")
+    return torch
+
+
+def make_config(model, M: int, N: int, timestep: float, settings: SolverSettings,
+                loop_mode: int = 0) -> _lib.GatoConfig:
+    model_id, params = device_model(model)
+    cfg = _lib.GatoConfig()
+    cfg.abi_version = _lib.ABI_VERSION
+    cfg.model_id = model_id
+    cfg.batch = M
+    cfg.horizon = N
+    cfg.state_dim = model.state_dim
+    cfg.control_dim = model.control_dim
+    cfg.force_dim = model.force_dim
+    cfg.max_sqp_iterations = settings.max_sqp_iterations
+    cfg.pcg_max_iterations = settings.pcg.max_iterations or 0
+    cfg.num_shrinks = settings.line_search.num_shrinks
+    cfg.regularize_r = int(settings.regularize_r)
+    cfg.pcg_retry_limit = settings.pcg_retry_limit
+    cfg.loop_mode = loop_mode
+    cfg.timestep = float(timestep)
+    cfg.pcg_tolerance = settings.pcg.tolerance
+    cfg.mu = settings.line_search.mu
+    cfg.beta = settings.line_search.beta
+    cfg.rho_min = settings.rho_min
+    cfg.rho_max = settings.rho_max
+    cfg.rho_factor = settings.rho_factor
+    cfg.step_tolerance = math.nan if settings.step_tolerance is None else settings.step_tolerance
+    cfg.feasibility_tolerance = settings.feasibility_tolerance
+    for i in range(8):
+        cfg.model_params[i] = float(params[i])
+    return cfg
+
+
+class BatchEngine:
+    """gato_create + gato_bind for one configuration; solve() is H2D -> gato_solve -> D2H."""
+
+    def __init__(self, model, M: int, N: int, timestep: float, settings: SolverSettings,
+                 device: int | None = None, loop_mode: int = 0):
+        torch = _torch()
+        self.lib = _lib.load()
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.model, self.M, self.N = model, M, N
+        self.settings = settings
+        n, m, fd = model.state_dim, model.control_dim, model.force_dim
+        self.shapes = {
+            "x_start": (M, n), "goal": (M, N + 1, n), "Q": (M, n, n), "R": (M, m, m),
+            "QN": (M, n, n), "force": (M, N, fd), "rho_init": (M,),
+            "X": (M, N + 1, n), "U": (M, N, m),
+        }
+        max_it = settings.max_sqp_iterations
+        with torch.cuda.device(self.device):
+            self.dev = {k: torch.zeros(s, dtype=torch.float64, device=self.device)
+                        for k, s in self.shapes.items()}
+            self.dev["trace"] = torch.zeros((M, max_it, _lib.TRACE_WORDS), dtype=torch.float64,
+                                            device=self.device)
+            self.dev["info"] = torch.zeros((M, _lib.INFO_WORDS), dtype=torch.int32, device=self.device)
+            self.pin_in = {k: torch.zeros(s, dtype=torch.float64).pin_memory()
+                           for k, s in self.shapes.items()}
+            self.pin_out = {k: torch.zeros_like(self.dev[k], device="cpu").pin_memory()
+                            for k in ("X", "U", "trace", "info")}
+            self.stream = torch.cuda.Stream(device=self.device)
+            cfg = make_config(model, M, N, timestep, settings, loop_mode)
+            handle = C.c_void_p()
+            rc = self.lib.gato_create(C.byref(cfg), C.byref(handle))
+            self.handle = handle
+            if rc != 0:
+                msg = self.lib.gato_last_error(handle).decode() if handle else "gato_create failed"
+                if handle:
+                    self.lib.gato_destroy(handle)
+                self.handle = None
+                raise RuntimeError(f"gato_create: {msg} (code {rc})")
+            bufs = _lib.GatoBuffers()
+            for name in ("x_start", "goal", "Q", "R", "QN", "force", "rho_init", "X", "U", "trace", "info"):
+                setattr(bufs, name, self.dev[name].data_ptr())
+            self._check(self.lib.gato_bind(self.handle, C.byref(bufs)), "gato_bind")
+
+    # -- plumbing --------------------------------------------------------------- #
+    def _check(self, rc: int, what: str):
+        if rc != 0:
+            raise RuntimeError(f"{what}: {self.lib.gato_last_error(self.handle).decode()} (code {rc})")
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.torch.cuda.synchronize(self.device)
+            self.lib.gato_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def loop_mode(self) -> int:
+        return int(self.lib.gato_loop_mode(self.handle))
+
+    # -- staged steps (all asynchronous on self.stream) ---------------------------- #
+    def upload(self, batch: PackedBatch, fields=INPUT_FIELDS):
+        """Host -> pinned -> device for the named inputs."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            for name in fields:
+                src = np.ascontiguousarray(getattr(batch, name), dtype=np.float64)
+                if src.shape != self.shapes[name]:
+                    raise ValueError(f"{name}: expected shape {self.shapes[name]}, got {src.shape}")
+                self.pin_in[name].numpy()[...] = src
+                self.dev[name].copy_(self.pin_in[name], non_blocking=True)
+
+    def launch(self):
+        """gato_solve on the engine stream; loops on the device until every solve terminated."""
+        self._check(self.lib.gato_solve(self.handle, C.c_void_p(self.stream.cuda_stream)), "gato_solve")
+
+    def finish(self):
+        """Loop modes without a device-side WHILE: run extra passes if a PCG retry used one."""
+        if self.loop_mode == 1:
+            return
+        pending = C.c_int32(0)
+        stream = C.c_void_p(self.stream.cuda_stream)
+        guard = self.settings.max_sqp_iterations * (self.settings.pcg_retry_limit + 1) + 1
+        while guard > 0:
+            self._check(self.lib.gato_pending(self.handle, stream, C.byref(pending)), "gato_pending")
+            if pending.value == 0:
+                break
+            self._check(self.lib.gato_resume(self.handle, stream, 1), "gato_resume")
+            guard -= 1
+
+    def download(self) -> PackedResult:
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            for name in ("X", "U", "trace", "info"):
+                self.pin_out[name].copy_(self.dev[name], non_blocking=True)
+        self.stream.synchronize()
+        ms = C.c_float(0.0)
+        self._check(self.lib.gato_last_solve_ms(self.handle, C.byref(ms)), "gato_last_solve_ms")
+        return PackedResult(self.pin_out["X"].numpy().copy(), self.pin_out["U"].numpy().copy(),
+                            self.pin_out["trace"].numpy().copy(), self.pin_out["info"].numpy().copy(),
+                            float(ms.value))
+
+    def solve(self, batch: PackedBatch) -> PackedResult:
+        """The end-to-end call: host inputs in, host results out."""
+        self.upload(batch)
+        self.launch()
+        self.finish()
+        return self.download()
+
+    def shift_warm_start(self):
+        """X, U <- shifted one knot left with the tail duplicated, on the device (mpc.py:85-89)."""
+        self._check(self.lib.gato_shift_warm_start(self.handle, C.c_void_p(self.stream.cuda_stream)),
+                    "gato_shift_warm_start")
+
+    def launch_count(self) -> int:
+        self.stream.synchronize()
+        return int(self.lib.gato_launch_count(self.handle))
+
+    def scratch(self, name: str) -> np.ndarray:
+        """Copy an internal stage array to the host (parity tests)."""
+        torch = self.torch
+        ptr, count = C.c_void_p(), C.c_int64()
+        self._check(self.lib.gato_scratch(self.handle, name.encode(), C.byref(ptr), C.byref(count)),
+                    "gato_scratch")
+        self.stream.synchronize()
+        is_int = name in ("si", "pcg_iters")
+        dtype, width = (np.int32, 4) if is_int else (np.float64, 8)
+        if name == "counters":
+            dtype, width = np.uint32, 4
+        out = np.empty(count.value, dtype=dtype)
+        self._check(self.lib.gato_read_scratch(self.handle, name.encode(), C.c_void_p(out.ctypes.data),
+                                               count.value * width), "gato_read_scratch")
+        return out
+
+
+# ------------------------------------------------------------------------------------
+# stateless operators (dynamics.step_many / step_jacobians_many / blocktri.pcg on the GPU)
+# ------------------------------------------------------------------------------------
+
+def _dev(torch, arr, dtype=None):
+    return torch.as_tensor(np.ascontiguousarray(arr, dtype=dtype or np.float64)).cuda()
+
+
+def step_many(model, X, U, h: float, F) -> np.ndarray:
+    """Row-wise RK4 steps on the GPU (dynamics.py:805-816)."""
+    torch = _torch()
+    lib = _lib.load()
+    model_id, params = device_model(model)
+    X = np.ascontiguousarray(X, dtype=float)
+    rows = X.shape[0]
+    dX, dU, dF = _dev(torch, X), _dev(torch, U), _dev(torch, F)
+    out = torch.empty_like(dX)
+    p = (C.c_double * 8)(*params)
+    rc = lib.gato_step_many(model_id, p, rows, dX.data_ptr(), dU.data_ptr(), dF.data_ptr(), float(h),
+                            out.data_ptr(), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"gato_step_many failed ({rc})")
+    return out.cpu().numpy()
+
+
+def step_jacobians_many(model, X, U, h: float, F):
+    """Row-wise exact RK4 Jacobians on the GPU (dynamics.py:774-802)."""
+    torch = _torch()
+    lib = _lib.load()
+    model_id, params = device_model(model)
+    X = np.ascontiguousarray(X, dtype=float)
+    rows, n = X.shape
+    m = model.control_dim
+    dX, dU, dF = _dev(torch, X), _dev(torch, U), _dev(torch, F)
+    A = torch.empty((rows, n, n), dtype=torch.float64, device="cuda")
+    B = torch.empty((rows, n, m), dtype=torch.float64, device="cuda")
+    p = (C.c_double * 8)(*params)
+    rc = lib.gato_step_jacobians_many(model_id, p, rows, dX.data_ptr(), dU.data_ptr(), dF.data_ptr(),
+                                      float(h), A.data_ptr(), B.data_ptr(),
+                                      C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"gato_step_jacobians_many failed ({rc})")
+    return A.cpu().numpy(), B.cpu().numpy()
+
+
+def pcg_batched(S_diag, S_off, gamma, P_diag, P_off, tolerance: float, max_iterations: int | None = None):
+    """Batched PCG on explicit block-tridiagonal systems (blocktri.py:123-173).
+
+    S_diag, P_diag: (systems, nb, bd, bd); S_off, P_off: (systems, nb-1, bd, bd);
+    gamma: (systems, nb*bd).  Returns (lam, iterations, converged, status, residual)."""
+    torch = _torch()
+    lib = _lib.load()
+    S_diag = np.ascontiguousarray(S_diag, dtype=float)
+    systems, nb, bd, _ = S_diag.shape
+    d = [_dev(torch, a) for a in (S_diag, S_off, gamma, P_diag, P_off)]
+    lam = torch.empty((systems, nb * bd), dtype=torch.float64, device="cuda")
+    its = torch.empty(systems, dtype=torch.int32, device="cuda")
+    conv = torch.empty(systems, dtype=torch.int32, device="cuda")
+    status = torch.empty(systems, dtype=torch.int32, device="cuda")
+    res = torch.empty(systems, dtype=torch.float64, device="cuda")
+    rc = lib.gato_pcg_batched(systems, nb, bd, *(t.data_ptr() for t in d), float(tolerance),
+                              int(max_iterations or 0), lam.data_ptr(), its.data_ptr(), conv.data_ptr(),
+                              status.data_ptr(), res.data_ptr(),
+                              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"gato_pcg_batched failed ({rc})")
+    return (lam.cpu().numpy(), its.cpu().numpy(), conv.cpu().numpy().astype(bool), status.cpu().numpy(),
+            res.cpu().numpy())
