@@ -152,6 +152,11 @@ int64_t gato_launch_count(const gato_handle* h);
 /* device time of the last gato_solve in milliseconds, measured with CUDA events on the
  * launching stream; synchronises on the end event */
 int gato_last_solve_ms(gato_handle* h, float* ms);
+/* gato_solve with CUDA events between the kernels of every pass (plain stream launches):
+ * ms[0..5] = hessinv, linearize, schur, pcg, linesearch, update totals; ms[6] prologue; ms[7] all. */
+int gato_solve_profiled(gato_handle* h, void* stream, float* ms);
+/* sustained fp64 FMA throughput of the current GPU in TFLOP/s (roofline denominator R1) */
+int gato_measure_fp64_peak(double* tflops);
 const char* gato_last_error(const gato_handle* h);
 void gato_destroy(gato_handle* h);
 

@@ -53,6 +53,8 @@ EXPORTS = {
     "gato_read_scratch": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64]),
     "gato_launch_count": (C.c_int64, [C.c_void_p]),
     "gato_last_solve_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    "gato_solve_profiled": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_float)]),
+    "gato_measure_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "gato_last_error": (C.c_char_p, [C.c_void_p]),
     "gato_destroy": (None, [C.c_void_p]),
     "gato_step_many": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int64, C.c_void_p,

@@ -266,4 +266,20 @@ __global__ void __launch_bounds__(256) k_pcg_explicit(int nb, int bd, const doub
   }
 }
 
+// 16 independent DFMA chains per thread, register resident: fp64 pipe throughput probe.
+__global__ void __launch_bounds__(256) k_fp64_peak(double* sink, int iters, double m) {
+  double a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = 1.0 + 1e-9 * (threadIdx.x + i);
+  const double c = 1e-12;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = fma(a[i], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i];
+  if (s == 123.456) sink[threadIdx.x] = s;
+}
+
 }  // namespace gato

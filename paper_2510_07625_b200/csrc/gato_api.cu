@@ -91,16 +91,24 @@ int dev_alloc(gato_handle* h, const char* name, T** out, int64_t count) {
 }
 
 // one SQP pass: six launches
-int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond) {
+// `marks`, when given, receives one event before each of the six launches and one after the last
+int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond, cudaEvent_t* marks = nullptr) {
   const SolveParams& P = h->P;
   RowView V{P.X, P.U, P.force, P.N, P.si};
+  if (marks) CK(cudaEventRecord(marks[0], s));
   CK(h->ops.hessinv(P, s));
+  if (marks) CK(cudaEventRecord(marks[1], s));
   CK(h->ops.linearize(V, P.mp, P.h, (int64_t)P.M * P.N, P.A, P.B, P.e, s));
+  if (marks) CK(cudaEventRecord(marks[2], s));
   CK(h->ops.schur(P, s));
+  if (marks) CK(cudaEventRecord(marks[3], s));
   CK(h->ops.pcg(P, s));
+  if (marks) CK(cudaEventRecord(marks[4], s));
   CK(h->ops.linesearch(P, 0, s));
+  if (marks) CK(cudaEventRecord(marks[5], s));
   k_update<<<P.M, 128, 0, s>>>(P, h->ops.nx, h->ops.nu, h->cond, use_cond);
   CK(cudaGetLastError());
+  if (marks) CK(cudaEventRecord(marks[6], s));
   return GATO_OK;
 }
 
@@ -394,6 +402,71 @@ int64_t gato_launch_count(const gato_handle* h) {
 }
 
 int gato_loop_mode(const gato_handle* h) { return h ? h->loop_mode : 0; }
+
+/* Same work as gato_solve in plain stream-launch mode, with CUDA events between the six kernels of
+ * every pass: ms[0..5] = total device time of hessinv, linearize, schur, pcg, linesearch, update
+ * over the max_sqp_iterations passes, ms[6] = prologue, ms[7] = whole call. Synchronous. */
+int gato_solve_profiled(gato_handle* h, void* stream, float* ms) {
+  if (!h || !ms) return GATO_E_INVALID;
+  if (!h->bound) return GATO_E_UNBOUND;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int passes = h->P.max_it;
+  std::vector<cudaEvent_t> ev((size_t)passes * 7 + 2);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  CK(cudaEventRecord(ev[passes * 7], s));
+  int rc = enqueue_prologue(h, s);
+  for (int it = 0; rc == GATO_OK && it < passes; ++it) rc = enqueue_pass(h, s, 0, &ev[(size_t)it * 7]);
+  if (rc == GATO_OK) {
+    CK(cudaEventRecord(ev[passes * 7 + 1], s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < 8; ++k) ms[k] = 0.f;
+    for (int it = 0; it < passes; ++it)
+      for (int k = 0; k < 6; ++k) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, ev[it * 7 + k], ev[it * 7 + k + 1]));
+        ms[k] += t;
+      }
+    CK(cudaEventElapsedTime(&ms[6], ev[passes * 7], ev[0]));
+    CK(cudaEventElapsedTime(&ms[7], ev[passes * 7], ev[passes * 7 + 1]));
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+/* Sustained fp64 FMA throughput of this GPU (TFLOP/s, FMA = 2 flops), measured with a
+ * register-resident DFMA kernel: the R1 roofline denominator of SURVEY.md section 8d, which
+ * MEASURED_PEAKS.json does not carry. Synchronous; ~50 ms. */
+int gato_measure_fp64_peak(double* tflops) {
+  if (!tflops) return GATO_E_INVALID;
+  gato_handle* h = nullptr;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return GATO_E_CUDA;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* sink = nullptr;
+  if (cudaMalloc(&sink, sizeof(double) * 1024) != cudaSuccess) return GATO_E_NOMEM;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    k_fp64_peak<<<blocks, threads>>>(sink, iters, 1.0000001);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    const double flops = 2.0 * 16.0 * (double)iters * (double)blocks * threads;
+    if (rep > 0 && t > 0.f) best = fmax(best, flops / (t * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  (void)h;
+  if (cudaGetLastError() != cudaSuccess) return GATO_E_CUDA;
+  *tflops = best;
+  return GATO_OK;
+}
 
 int gato_last_solve_ms(gato_handle* h, float* ms) {
   if (!h || !ms) return GATO_E_INVALID;

@@ -226,6 +226,16 @@ class BatchEngine:
         self._check(self.lib.gato_shift_warm_start(self.handle, C.c_void_p(self.stream.cuda_stream)),
                     "gato_shift_warm_start")
 
+    KERNEL_FAMILIES = ("hessinv", "linearize", "schur", "pcg", "linesearch", "update", "prologue", "total")
+
+    def solve_profiled(self) -> dict:
+        """One solve in plain stream-launch mode with CUDA events between the kernels: device
+        milliseconds per kernel family, summed over the passes (inputs must be uploaded)."""
+        ms = (C.c_float * 8)()
+        self._check(self.lib.gato_solve_profiled(self.handle, C.c_void_p(self.stream.cuda_stream), ms),
+                    "gato_solve_profiled")
+        return dict(zip(self.KERNEL_FAMILIES, (float(v) for v in ms)))
+
     def launch_count(self) -> int:
         self.stream.synchronize()
         return int(self.lib.gato_launch_count(self.handle))
@@ -253,6 +263,16 @@ class BatchEngine:
 
 def _dev(torch, arr, dtype=None):
     return torch.as_tensor(np.ascontiguousarray(arr, dtype=dtype or np.float64)).cuda()
+
+
+def measure_fp64_peak() -> float:
+    """Sustained fp64 FMA TFLOP/s of the current GPU (register-resident DFMA probe)."""
+    _torch()
+    out = C.c_double(0.0)
+    rc = _lib.load().gato_measure_fp64_peak(C.byref(out))
+    if rc != 0:
+        raise RuntimeError(f"gato_measure_fp64_peak failed ({rc})")
+    return float(out.value)
 
 
 def step_many(model, X, U, h: float, F) -> np.ndarray:
