@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) k_pcg_explicit(int nb, int bd, const doub
   double* p = z + size;
   double* q = p + size;
   double* tmp = q + size;
-  double2* red = reinterpret_cast<double2*>(tmp + size + (size & 1));
+  double2* red = reinterpret_cast<double2*>(tmp + size);  // 6 * size doubles: always 16-byte aligned
   BlockReducer R{red, 0, (int)((blockDim.x + 31) >> 5)};
   double acc = 0.0;
   for (int i = threadIdx.x; i < size; i += blockDim.x) {

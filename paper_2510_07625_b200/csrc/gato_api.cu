@@ -526,7 +526,7 @@ int gato_pcg_batched(int32_t systems, int32_t nb, int32_t bd, const double* S_di
                      double* residual, void* stream) {
   if (systems < 1 || nb < 1 || bd < 1) return GATO_E_INVALID;
   const int size = nb * bd;
-  const size_t bytes = ((size_t)6 * size + (size & 1)) * 8 + 64 * 16;
+  const size_t bytes = (size_t)6 * size * 8 + 64 * 16;
   if (bytes > kMaxSmem) return GATO_E_INVALID;
   const int cap = max_iterations > 0 ? max_iterations : 10 * size;
   if (cudaFuncSetAttribute(k_pcg_explicit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)

@@ -262,7 +262,10 @@ class BatchEngine:
 # ------------------------------------------------------------------------------------
 
 def _dev(torch, arr, dtype=None):
-    return torch.as_tensor(np.ascontiguousarray(arr, dtype=dtype or np.float64)).cuda()
+    arr = np.ascontiguousarray(arr, dtype=dtype or np.float64)
+    if arr.size == 0:        # e.g. the off-diagonal stack of a single-block-row system
+        return torch.zeros(1, dtype=torch.float64, device="cuda")
+    return torch.as_tensor(arr).cuda()
 
 
 def measure_fp64_peak() -> float:
