@@ -22,11 +22,21 @@ pytestmark = pytest.mark.gpu
 TRAJ_TOL = 1e-4     # north star: relative error of the final trajectories
 
 
-def _decisive(ref_trace):
-    """Iterations whose accept decision is not on the merit plateau."""
-    merit = ref_trace[:, 1]
-    prev = np.concatenate([[np.inf], merit[:-1]])
-    return np.abs(prev - merit) > 1e-10 * np.maximum(1.0, np.abs(merit))
+def _first_decision_flip(got, ref):
+    """Index of the first iteration whose (alpha, accepted) differ, or len(ref)."""
+    for k in range(len(ref)):
+        same_alpha = (got[k, 3] == ref[k, 3]) or (np.isnan(got[k, 3]) and np.isnan(ref[k, 3]))
+        if not (same_alpha and got[k, 6] == ref[k, 6]):
+            return k
+    return len(ref)
+
+
+def _on_plateau(ref, k):
+    """The reference's own merit moves by less than 1e-8 |merit| at iteration k and the step is
+    tiny: there the candidate merits tie to rounding and the reference itself flips under 1e-13
+    input perturbations."""
+    prev = ref[k - 1, 1] if k > 0 else np.inf
+    return abs(prev - ref[k, 1]) <= 1e-8 * max(1.0, abs(ref[k, 1])) and ref[k, 7] <= 1e-3
 
 
 @pytest.mark.parametrize("name", ALL_CASES)
@@ -39,14 +49,14 @@ def test_solve_matches_reference_golden(name):
     assert rel_inf(res.X, g["X"]) <= TRAJ_TOL and rel_inf(res.U, g["U"]) <= TRAJ_TOL
     assert len(got) == len(ref), "SQP iteration count differs"
     assert res.converged == bool(g["converged"])
-    assert np.max(np.abs(got[:, 5] - ref[:, 5])) <= 1, "PCG iteration counts differ by more than 1"
     assert np.array_equal(got[:, 0], ref[:, 0])
-    keep = _decisive(ref) & ~np.isnan(ref[:, 3])
-    if keep.any() and len(ref) <= 10:
-        assert np.array_equal(got[keep, 3], ref[keep, 3]), "step lengths differ off the plateau"
-        assert np.array_equal(got[keep, 6], ref[keep, 6]), "accept flags differ off the plateau"
+    flip = _first_decision_flip(got, ref)
+    if flip < len(ref):
+        assert _on_plateau(ref, flip), f"step decision differs off the merit plateau at iteration {flip}"
+    upto = min(len(ref), flip + 1)      # quantities computed before the flipped decision still agree
+    assert np.max(np.abs(got[:upto, 5] - ref[:upto, 5])) <= 1, "PCG iteration counts differ by more than 1"
+    assert rel_inf(got[:upto, 4], ref[:upto, 4]) <= 1e-12, "rho trace"
     assert rel_inf(got[:, 1], ref[:, 1]) <= 1e-6, "merit trace"
-    assert rel_inf(got[:, 4], ref[:, 4]) <= 1e-12 or len(ref) > 10, "rho trace"
 
 
 def test_restart_at_solution_returns_one_record_and_untouched_iterate():
