@@ -64,7 +64,7 @@ struct gato_handle {
   bool graph_valid = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
-  int static_launches = 0;  // launches outside the pass loop
+  void* lin_scratch = nullptr;  // model-private linearisation scratch (iiwa14: per-stage link data)
 };
 
 namespace {
@@ -98,7 +98,7 @@ int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond, cudaEvent_t* mark
   if (marks) CK(cudaEventRecord(marks[0], s));
   CK(h->ops.hessinv(P, s));
   if (marks) CK(cudaEventRecord(marks[1], s));
-  CK(h->ops.linearize(V, P.mp, P.h, (int64_t)P.M * P.N, P.A, P.B, P.e, s));
+  CK(h->ops.linearize(V, P.mp, P.h, (int64_t)P.M * P.N, P.A, P.B, P.e, h->lin_scratch, s));
   if (marks) CK(cudaEventRecord(marks[2], s));
   CK(h->ops.schur(P, s));
   if (marks) CK(cudaEventRecord(marks[3], s));
@@ -209,8 +209,8 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
     set_error(h, "batch, horizon, max_sqp_iterations must be >= 1 and timestep > 0");
     return GATO_E_INVALID;
   }
-  if ((cfg->horizon + 1) * (nx / 2) > 1024) {
-    set_error(h, "horizon too long: (N+1)*n/2 must be <= 1024 rows-pairs per solve");
+  if (cfg->horizon + 1 > kPcgMaxThreads) {
+    set_error(h, "horizon too long: the PCG kernel runs one thread per block row, N + 1 <= 256");
     return GATO_E_INVALID;
   }
   SolveParams& P = h->P;
@@ -257,6 +257,15 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   ALLOC(counters, 8);
 #undef ALLOC
   if (rc != GATO_OK) return rc;
+  {
+    const size_t bytes = h->ops.lin_scratch_bytes(M * N);
+    if (bytes) {
+      unsigned char* p = nullptr;
+      rc = dev_alloc(h, "lin_scratch", &p, (int64_t)bytes);
+      if (rc != GATO_OK) return rc;
+      h->lin_scratch = p;
+    }
+  }
   // step lengths beta^-c, computed on the host exactly as sqp.py:51-52 (libm pow)
   std::vector<double> alphas(P.C);
   for (int c = 0; c < P.C; ++c) alphas[c] = pow(cfg->beta, -(double)c);
@@ -516,7 +525,15 @@ int gato_step_jacobians_many(int32_t model_id, const double* model_params, int64
   // operator mode: one "solve" whose N = rows, so row r is addressed as (b = 0, k = r); the
   // defect output is off, so the (N+1)-th state row of the solve layout is never read.
   RowView V{X, U, F, (int)rows, nullptr};
-  cudaError_t err = ops.linearize(V, mp, timestep, rows, A, B, nullptr, static_cast<cudaStream_t>(stream));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  void* scratch = nullptr;
+  const size_t bytes = ops.lin_scratch_bytes(rows);
+  if (bytes && cudaMalloc(&scratch, bytes) != cudaSuccess) return GATO_E_NOMEM;
+  cudaError_t err = ops.linearize(V, mp, timestep, rows, A, B, nullptr, scratch, s);
+  if (scratch) {
+    cudaStreamSynchronize(s);   // operator entry point: scratch lives for this call only
+    cudaFree(scratch);
+  }
   return err == cudaSuccess ? GATO_OK : GATO_E_CUDA;
 }
 

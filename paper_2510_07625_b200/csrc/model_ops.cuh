@@ -12,8 +12,10 @@ constexpr size_t kMaxSmem = 227 * 1024;
 struct ModelOps {
   int nx, nu, nf;
   cudaError_t (*hessinv)(const SolveParams&, cudaStream_t);
+  // `scratch`: model-private device buffer of lin_scratch_bytes(rows) bytes (may be null if 0)
   cudaError_t (*linearize)(const RowView&, const ModelParams&, double, int64_t, double*, double*, double*,
-                           cudaStream_t);
+                           void* scratch, cudaStream_t);
+  size_t (*lin_scratch_bytes)(int64_t rows);
   cudaError_t (*schur)(const SolveParams&, cudaStream_t);
   cudaError_t (*pcg)(const SolveParams&, cudaStream_t);
   cudaError_t (*linesearch)(const SolveParams&, int, cudaStream_t);
@@ -34,30 +36,22 @@ cudaError_t launch_hessinv(const SolveParams& P, cudaStream_t s) {
 }
 
 template <class Mdl>
+size_t lin_scratch_bytes(int64_t rows) {
+  if constexpr (Mdl::ANALYTIC_JAC) return 0;
+  else return (size_t)rows * 4 * sizeof(iiwa::Stage);   // per-stage link data of every knot
+}
+
+template <class Mdl>
 cudaError_t launch_linearize(const RowView& V, const ModelParams& mp, double h, int64_t rows, double* A, double* B,
-                             double* e, cudaStream_t s) {
+                             double* e, void* scratch, cudaStream_t s) {
   if constexpr (Mdl::ANALYTIC_JAC) {
     const int threads = 64;
     k_linearize_simple<Mdl><<<(unsigned)((rows + threads - 1) / threads), threads, 0, s>>>(V, mp, h, rows, A, B, e);
   } else {
-    static int G = 0;
-    if (!G) {
-      G = env_int("GATO_LIN_GROUP", 16);
-      if (G != 8 && G != 16 && G != 32) G = 16;
-    }
-    const int threads = 128;
-    const int groups = threads / G;
-    const size_t smem = (size_t)groups * 4 * sizeof(iiwa::Stage);
-    const unsigned grid = (unsigned)((rows + groups - 1) / groups);
-    cudaError_t err = cudaSuccess;
-    if (G == 8) {
-      k_linearize_iiwa<8><<<grid, threads, smem, s>>>(V, h, rows, A, B, e);
-    } else if (G == 16) {
-      k_linearize_iiwa<16><<<grid, threads, smem, s>>>(V, h, rows, A, B, e);
-    } else {
-      k_linearize_iiwa<32><<<grid, threads, smem, s>>>(V, h, rows, A, B, e);
-    }
-    if (err != cudaSuccess) return err;
+    iiwa::Stage* stages = static_cast<iiwa::Stage*>(scratch);
+    k_lin_primal_iiwa<0><<<(unsigned)((rows + 63) / 64), 64, 0, s>>>(V, h, rows, stages, e);
+    k_lin_tangent_iiwa<0><<<(unsigned)((rows + kLinKnotsPerCta - 1) / kLinKnotsPerCta), 128, 0, s>>>(V, h, rows, stages,
+                                                                                                   A, B);
   }
   return cudaGetLastError();
 }
@@ -73,32 +67,21 @@ cudaError_t launch_schur(const SolveParams& P, cudaStream_t s) {
 
 template <int NX>
 size_t pcg_smem_bytes(int N, bool mats) {
-  const int nb = N + 1;
-  const size_t vpad = ((size_t)nb * NX + 1) & ~(size_t)1;
-  size_t bytes = 3 * vpad * 8 + 64 * 16;
-  if (mats) bytes += ((size_t)N * NX * NX + (size_t)nb * (NX * (NX + 1) / 2)) * 8;
-  return bytes;
+  using L = PcgLayout<NX>;
+  return L::vec_bytes(N + 1) + (mats ? L::mat_bytes(N) : 0);
 }
 
 template <class Mdl>
 cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU;
-  const int need = (P.N + 1) * (NX / 2);
-  const int threads = ((need + 31) / 32) * 32;
+  const int threads = ((P.N + 1 + 31) / 32) * 32;
+  if (threads > kPcgMaxThreads) return cudaErrorInvalidConfiguration;
   const size_t with_mats = pcg_smem_bytes<NX>(P.N, true);
   const bool force_global = env_int("GATO_PCG_GLOBAL", 0) != 0;
-  if (threads <= 512 && with_mats <= kMaxSmem && !force_global) {
-    auto kern = k_pcg<NX, NU, true, 512>;
-    kern<<<P.M, threads, with_mats, s>>>(P);
-  } else if (threads <= 512) {
-    auto kern = k_pcg<NX, NU, false, 512>;
-    kern<<<P.M, threads, pcg_smem_bytes<NX>(P.N, false), s>>>(P);
-  } else if (threads <= 1024) {
-    auto kern = k_pcg<NX, NU, false, 1024>;
-    const size_t bytes = pcg_smem_bytes<NX>(P.N, false);
-    kern<<<P.M, threads, bytes, s>>>(P);
+  if (with_mats <= kMaxSmem && !force_global) {
+    k_pcg<NX, NU, true><<<P.M, threads, with_mats, s>>>(P);
   } else {
-    return cudaErrorInvalidConfiguration;
+    k_pcg<NX, NU, false><<<P.M, threads, pcg_smem_bytes<NX>(P.N, false), s>>>(P);
   }
   return cudaGetLastError();
 }
@@ -124,30 +107,23 @@ template <class Mdl>
 cudaError_t prepare_attrs(const SolveParams& P) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU;
   cudaError_t err;
-  if constexpr (!Mdl::ANALYTIC_JAC) {
-    err = cudaFuncSetAttribute(k_linearize_iiwa<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(16 * 4 * sizeof(iiwa::Stage)));
-    if (err != cudaSuccess) return err;
-  }
   err = cudaFuncSetAttribute(k_schur<NX, NU, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(4 * sizeof(SchurSmem<NX, NU>)));
   if (err != cudaSuccess) return err;
   const size_t with_mats = pcg_smem_bytes<NX>(P.N, true);
   if (with_mats <= kMaxSmem) {
-    err = cudaFuncSetAttribute(k_pcg<NX, NU, true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_mats);
+    err = cudaFuncSetAttribute(k_pcg<NX, NU, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_mats);
     if (err != cudaSuccess) return err;
   }
   const size_t bytes = pcg_smem_bytes<NX>(P.N, false);
-  err = cudaFuncSetAttribute(k_pcg<NX, NU, false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (err != cudaSuccess) return err;
-  err = cudaFuncSetAttribute(k_pcg<NX, NU, false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  return err;
+  if (bytes > 48 * 1024) return cudaErrorInvalidConfiguration;
+  return cudaSuccess;
 }
 
 template <class Mdl>
 ModelOps make_ops() {
   return ModelOps{Mdl::NX,           Mdl::NU,           Mdl::NF,
-                  launch_hessinv<Mdl>, launch_linearize<Mdl>, launch_schur<Mdl>,
+                  launch_hessinv<Mdl>, launch_linearize<Mdl>, lin_scratch_bytes<Mdl>, launch_schur<Mdl>,
                   launch_pcg<Mdl>,     launch_linesearch<Mdl>, launch_step_rows<Mdl>, prepare_attrs<Mdl>};
 }
 

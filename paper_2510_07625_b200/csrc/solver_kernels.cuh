@@ -242,100 +242,100 @@ __global__ void k_linearize_simple(RowView V, ModelParams mp, double h, int64_t 
 }
 
 // -----------------------------------------------------------------------------------------
-// k_linearize_iiwa: a group of G lanes per knot.  Lane 0 of the group runs the four primal
-// RK4 stages and leaves the per-stage link data in shared memory; then every lane carries one
-// tangent direction (14 state + 7 control columns) through the four stages: column d of
-// [A | B] is the exact derivative of the RK4 map along that direction -- the same chain rule
-// as dynamics.py:774-802, evaluated as Jacobian-vector products so no n x n x n product and
-// no cross-lane traffic is needed.
+// iiwa14 linearisation, two kernels.
+//
+// k_lin_primal_iiwa : one thread per knot runs the four primal RK4 stages, writes the defect
+//                     e_k and leaves the per-stage link data (iiwa::Stage x 4) in global scratch.
+// k_lin_tangent_iiwa: one thread per (knot, direction), 14 state + 7 control directions.  Each
+//                     thread carries its tangent through the four stages: column d of [A | B] is
+//                     the exact derivative of the RK4 map along that direction -- the chain rule
+//                     of dynamics.py:774-802 evaluated as Jacobian-vector products, so there is no
+//                     n x n x n product and no cross-thread traffic.  The 21 direction threads of
+//                     a knot read the same stage record (L1 broadcast).
 // -----------------------------------------------------------------------------------------
-template <int G>
-__global__ void __launch_bounds__(128) k_linearize_iiwa(RowView V, double h, int64_t rows, double* __restrict__ A,
-                                                        double* __restrict__ B, double* __restrict__ e) {
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(64) k_lin_primal_iiwa(RowView V, double h, int64_t rows,
+                                                        iiwa::Stage* __restrict__ stages, double* __restrict__ e) {
   constexpr int NX = 14, NU = 7, NF = 3;
-  extern __shared__ double lin_smem[];
-  const int gid = threadIdx.x / G, gl = threadIdx.x % G;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / G) + gid;
-  bool valid = r < rows;
-  int64_t b = 0, k = 0;
-  if (valid) {
-    b = r / V.N;
-    k = r % V.N;
-    if (V.si && !V.si[b * SI_WORDS + SI_ACTIVE]) valid = false;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t b = r / V.N, k = r % V.N;
+  if (V.si && !V.si[b * SI_WORDS + SI_ACTIVE]) return;
+  const double* xg = V.X + (b * (V.N + 1) + k) * NX;
+  double x[NX], u[NU], f[NF], kk[NX], xs[NX], ksum[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    x[i] = xg[i];
+    xs[i] = x[i];
+    ksum[i] = 0.0;
   }
-  iiwa::Stage* st = reinterpret_cast<iiwa::Stage*>(lin_smem) + gid * 4;
-  double f[NF] = {0, 0, 0};
-  if (valid) {
 #pragma unroll
-    for (int i = 0; i < NF; ++i) f[i] = V.F[r * NF + i];
-  }
-  if (valid && gl == 0) {
-    const double* xg = V.X + (b * (V.N + 1) + k) * NX;
-    double x[NX], u[NU], kk[NX], xs[NX], ksum[NX];
+  for (int i = 0; i < NU; ++i) u[i] = V.U[r * NU + i];
 #pragma unroll
-    for (int i = 0; i < NX; ++i) x[i] = xg[i];
-#pragma unroll
-    for (int i = 0; i < NU; ++i) u[i] = V.U[r * NU + i];
-    iiwa::forward_dynamics<true>(x, u, f, kk, &st[0]);
+  for (int i = 0; i < NF; ++i) f[i] = V.F[r * NF + i];
+  iiwa::Stage* st = stages + r * 4;
+#pragma unroll 1
+  for (int s = 0; s < 4; ++s) {
+    iiwa::forward_dynamics<true>(xs, u, f, kk, st + s);
+    const double wgt = (s == 0 || s == 3) ? 1.0 : 2.0;
+    const double lead = (s == 2) ? h : 0.5 * h;   // offset of the NEXT stage point
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
-      ksum[i] = kk[i];
-      xs[i] = x[i] + 0.5 * h * kk[i];
-    }
-    iiwa::forward_dynamics<true>(xs, u, f, kk, &st[1]);
-#pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      ksum[i] = ksum[i] + 2.0 * kk[i];
-      xs[i] = x[i] + 0.5 * h * kk[i];
-    }
-    iiwa::forward_dynamics<true>(xs, u, f, kk, &st[2]);
-#pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      ksum[i] = ksum[i] + 2.0 * kk[i];
-      xs[i] = x[i] + h * kk[i];
-    }
-    iiwa::forward_dynamics<true>(xs, u, f, kk, &st[3]);
-    if (e) {
-      const double* xn = xg + NX;
-#pragma unroll
-      for (int i = 0; i < NX; ++i) e[r * NX + i] = (x[i] + (h / 6.0) * (ksum[i] + kk[i])) - xn[i];
+      ksum[i] = ksum[i] + wgt * kk[i];
+      xs[i] = x[i] + lead * kk[i];
     }
   }
-  __syncwarp();
-  if (!valid) return;
-  for (int d = gl; d < NX + NU; d += G) {
-    const int du = (d >= NX) ? d - NX : -1;
-    double dx[NX], dk[NX], acc[NX];
+  if (e) {
+    const double* xn = xg + NX;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) dx[i] = (i == d) ? 1.0 : 0.0;
-    iiwa::tangent(&st[0], f, dx, du, dk);
+    for (int i = 0; i < NX; ++i) e[r * NX + i] = (x[i] + (h / 6.0) * ksum[i]) - xn[i];
+  }
+}
+
+constexpr int kLinDirs = 21;          // 14 state + 7 control directions
+constexpr int kLinKnotsPerCta = 6;    // 126 of 128 threads active
+
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(128) k_lin_tangent_iiwa(RowView V, double h, int64_t rows,
+                                                          const iiwa::Stage* __restrict__ stages,
+                                                          double* __restrict__ A, double* __restrict__ B) {
+  constexpr int NX = 14, NU = 7, NF = 3;
+  const int t = threadIdx.x;
+  if (t >= kLinKnotsPerCta * kLinDirs) return;
+  const int64_t r = (int64_t)blockIdx.x * kLinKnotsPerCta + t / kLinDirs;
+  const int d = t % kLinDirs;
+  if (r >= rows) return;
+  if (V.si && !V.si[(r / V.N) * SI_WORDS + SI_ACTIVE]) return;
+  double f[NF];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) f[i] = V.F[r * NF + i];
+  const int du = (d >= NX) ? d - NX : -1;
+  const iiwa::Stage* st = stages + r * 4;
+  double dx[NX], dk[NX], acc[NX];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    dx[i] = (i == d) ? 1.0 : 0.0;
+    acc[i] = 0.0;
+  }
+#pragma unroll 1
+  for (int s = 0; s < 4; ++s) {
+    iiwa::tangent(st + s, f, dx, du, dk);
+    const double wgt = (s == 0 || s == 3) ? 1.0 : 2.0;
+    const double lead = (s == 2) ? h : 0.5 * h;
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
-      acc[i] = dk[i];
-      dx[i] = ((i == d) ? 1.0 : 0.0) + 0.5 * h * dk[i];
+      acc[i] = acc[i] + wgt * dk[i];
+      dx[i] = ((i == d) ? 1.0 : 0.0) + lead * dk[i];
     }
-    iiwa::tangent(&st[1], f, dx, du, dk);
+  }
+  if (d < NX) {
+    double* Ag = A + r * NX * NX;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      acc[i] = acc[i] + 2.0 * dk[i];
-      dx[i] = ((i == d) ? 1.0 : 0.0) + 0.5 * h * dk[i];
-    }
-    iiwa::tangent(&st[2], f, dx, du, dk);
+    for (int i = 0; i < NX; ++i) Ag[i * NX + d] = ((i == d) ? 1.0 : 0.0) + (h / 6.0) * acc[i];
+  } else {
+    double* Bg = B + r * NX * NU;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      acc[i] = acc[i] + 2.0 * dk[i];
-      dx[i] = ((i == d) ? 1.0 : 0.0) + h * dk[i];
-    }
-    iiwa::tangent(&st[3], f, dx, du, dk);
-    if (d < NX) {
-      double* Ag = A + r * NX * NX;
-#pragma unroll
-      for (int i = 0; i < NX; ++i) Ag[i * NX + d] = ((i == d) ? 1.0 : 0.0) + (h / 6.0) * (acc[i] + dk[i]);
-    } else {
-      double* Bg = B + r * NX * NU;
-#pragma unroll
-      for (int i = 0; i < NX; ++i) Bg[i * NU + du] = (h / 6.0) * (acc[i] + dk[i]);
-    }
+    for (int i = 0; i < NX; ++i) Bg[i * NU + du] = (h / 6.0) * acc[i];
   }
 }
 
@@ -510,16 +510,26 @@ __global__ void __launch_bounds__(WARPS * 32) k_schur(SolveParams P) {
 }
 
 // -----------------------------------------------------------------------------------------
-// k_pcg: one CTA per solve.  Thread (k, i) owns rows i and i + NX/2 of block row k.
-//   - its two rows of the diagonal block S_kk live in registers for the whole solve,
-//   - the sub-diagonal blocks phi_k and the packed D_k^-1 live in shared memory (or stay in
-//     global memory when the horizon is too long for 227 KB: SMEM_MATS = false),
-//   - Phi^-1 r is applied in factored form  z_k = D_k^-1 (r_k - phi_{k-1} w_{k-1} - phi_k^T w_{k+1}),
-//     w = D^-1 r, algebraically identical to the explicit stair blocks of qpform.py:355-356,
-//   - dot products: fixed xor-shuffle tree inside a warp, fixed-order sum over warps
-//     (bitwise reproducible, independent of batch position),
-//   - stop test on the recurrence residual ||r||_2 (the reference recomputes ||S lam - gamma||,
-//     blocktri.py:165; SURVEY.md 3.3 measured identical iteration counts in fp64).
+// k_pcg: one CTA per solve, ONE THREAD PER BLOCK ROW ("fat threads").
+//
+// Thread k owns block row k of S lam = gamma: its 14 entries of lam, r, p live in registers and
+// it needs, per matvec, its own diagonal block plus the two neighbouring sub-diagonal blocks.
+// Why one thread per block row: the matvecs are bound by shared-memory wavefronts, not by the
+// fp64 pipe.  With a thread per row every lane re-reads the same 42 vector entries (broadcast
+// loads that cost as many wavefronts as the matrix itself) and phi_k^T needs strided column
+// reads; a thread that owns the whole block row reads every matrix element exactly once with
+// 16-byte row loads, applies phi_k^T by rows (14 accumulators), and uses each element of the
+// symmetric blocks S_kk and D_k^-1 for two FMAs from packed lower-triangular storage.
+//   shared memory: phi_k (row-major, block stride padded to 2 mod 4 doubles so that the lanes of
+//   a quarter-warp hit distinct 16-byte bank groups), packed S_kk, packed D_k^-1, two exchange
+//   vectors.  N = 64, n = 14: 222 KB of the 227 KB.  Longer horizons read the blocks from
+//   global memory (SMEM_MATS = false).
+//   Phi^-1 r is applied in factored form  z_k = D_k^-1 (r_k - phi_{k-1} w_{k-1} - phi_k^T w_{k+1}),
+//   w = D^-1 r, algebraically identical to the explicit stair blocks of qpform.py:355-356.
+//   Dot products: fixed xor-shuffle tree inside a warp, fixed-order sum over warps (bitwise
+//   reproducible, independent of batch position).  Stop test on the recurrence residual ||r||_2
+//   (the reference recomputes ||S lam - gamma||, blocktri.py:165; SURVEY.md 3.3 measured
+//   identical iteration counts in fp64).
 // Then the primal step (qpform.py:375-397), ||dZ||_inf, the violation of the current iterate
 // (sqp.py:254) and the tolerance exit (sqp.py:256-272).
 // -----------------------------------------------------------------------------------------
@@ -578,10 +588,119 @@ struct BlockReducer {
   }
 };
 
-template <int NX, int NU, bool SMEM_MATS, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) k_pcg(SolveParams P) {
-  constexpr bool SD_REGS = (MAXT <= 512);  // 128 registers per thread available
-  constexpr int HN = NX / 2, TRI = NX * (NX + 1) / 2, BS = NX * NX;
+// smallest even m >= n with m / 2 odd: a block stride of m doubles puts consecutive lanes on
+// distinct 16-byte bank groups for 128-bit shared-memory loads
+__host__ __device__ constexpr int pad_stride(int n) {
+  int m = (n + 1) & ~1;
+  return ((m / 2) % 2 == 0) ? m + 2 : m;
+}
+
+template <int NX>
+struct PcgLayout {
+  static constexpr int BS = NX * NX, TRI = NX * (NX + 1) / 2;
+  static constexpr int BSP = pad_stride(BS), TRP = pad_stride(TRI);
+  static constexpr int VSTRIDE = NX;   // exchange vectors: NX doubles per block row (NX even)
+  __host__ __device__ static size_t vec_bytes(int nb) { return 2 * (size_t)(nb * NX + 2) * 8 + 64 * 16; }
+  __host__ __device__ static size_t mat_bytes(int N) {
+    return ((size_t)N * BSP + 2 * (size_t)(N + 1) * TRP) * 8;
+  }
+};
+
+// y += M v for a symmetric block in packed lower-triangular storage (row-major, 16-byte aligned)
+template <int NX>
+__device__ __forceinline__ void sym_apply_packed(const double* __restrict__ Mp, const double* v, double* y) {
+  const double2* M2 = reinterpret_cast<const double2*>(Mp);
+  double2 cur = make_double2(0.0, 0.0);
+  int idx = 0;
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+#pragma unroll
+    for (int j = 0; j <= i; ++j, ++idx) {
+      double m;
+      if ((idx & 1) == 0) {
+        cur = M2[idx >> 1];
+        m = cur.x;
+      } else {
+        m = cur.y;
+      }
+      if (j < i) {
+        y[i] = fma(m, v[j], y[i]);
+        y[j] = fma(m, v[i], y[j]);
+      } else {
+        y[i] = fma(m, v[i], y[i]);
+      }
+    }
+  }
+}
+// same for a full row-major block of which only the lower triangle is read
+template <int NX>
+__device__ __forceinline__ void sym_apply_full(const double* __restrict__ Mf, const double* v, double* y) {
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      const double m = Mf[i * NX + j];
+      if (j < i) {
+        y[i] = fma(m, v[j], y[i]);
+        y[j] = fma(m, v[i], y[j]);
+      } else {
+        y[i] = fma(m, v[i], y[i]);
+      }
+    }
+  }
+}
+// y += O v (row i of O against v) and y += O^T v (row j of O scaled by v[j]); O row-major
+template <int NX>
+__device__ __forceinline__ void off_apply_rows(const double* __restrict__ O, const double* v, double* y) {
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    const double2* r2 = reinterpret_cast<const double2*>(O + i * NX);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < NX / 2; ++j) {
+      const double2 a = r2[j];
+      acc = fma(a.x, v[2 * j], acc);
+      acc = fma(a.y, v[2 * j + 1], acc);
+    }
+    y[i] += acc;
+  }
+}
+template <int NX>
+__device__ __forceinline__ void off_apply_cols(const double* __restrict__ O, const double* v, double* y) {
+#pragma unroll
+  for (int j = 0; j < NX; ++j) {
+    const double2* r2 = reinterpret_cast<const double2*>(O + j * NX);
+    const double vj = v[j];
+#pragma unroll
+    for (int i = 0; i < NX / 2; ++i) {
+      const double2 a = r2[i];
+      y[2 * i] = fma(a.x, vj, y[2 * i]);
+      y[2 * i + 1] = fma(a.y, vj, y[2 * i + 1]);
+    }
+  }
+}
+template <int NX>
+__device__ __forceinline__ void vec_store(double* dst, const double* v) {
+#pragma unroll
+  for (int j = 0; j < NX / 2; ++j) reinterpret_cast<double2*>(dst)[j] = make_double2(v[2 * j], v[2 * j + 1]);
+}
+template <int NX>
+__device__ __forceinline__ void vec_load(const double* src, double* v) {
+#pragma unroll
+  for (int j = 0; j < NX / 2; ++j) {
+    const double2 a = reinterpret_cast<const double2*>(src)[j];
+    v[2 * j] = a.x;
+    v[2 * j + 1] = a.y;
+  }
+}
+
+constexpr int kPcgMaxThreads = 256;
+
+template <int NX, int NU, bool SMEM_MATS>
+__global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
+  static_assert(NX % 2 == 0, "state = [positions, velocities]");
+  using L = PcgLayout<NX>;
+  constexpr int BS = L::BS, TRI = L::TRI;
   constexpr int HS = hinv_stride(NX, NU);
   const int b = blockIdx.x;
   int32_t* si = P.si + b * SI_WORDS;
@@ -598,160 +717,163 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg(SolveParams P) {
   }
   extern __shared__ __align__(16) double pcg_smem[];
   const int vlen = nb * NX;
-  const int vpad = (vlen + 1) & ~1;
-  double* vp = pcg_smem;       // search direction p
-  double* vr = vp + vpad;      // residual r, later r - t
-  double* vw = vr + vpad;      // w = D^-1 r
-  double2* red = reinterpret_cast<double2*>(vw + vpad);
+  double* vA = pcg_smem;                 // exchange buffer: w, later lambda
+  double* vB = vA + vlen + 2;            // exchange buffer: p
+  double2* red = reinterpret_cast<double2*>(vB + vlen + 2);
   double* mats = reinterpret_cast<double*>(red + 64);
-  const double* So;
-  const double* Di;
+  // block strides of the three matrix families as this kernel reads them
+  constexpr int OST = SMEM_MATS ? L::BSP : BS;
+  constexpr int SST = SMEM_MATS ? L::TRP : BS;     // S_kk: packed in smem, full (lower read) in global
+  constexpr int DST = SMEM_MATS ? L::TRP : TRI;    // D_k^-1: packed
+  const double *So, *Sd, *Di;
   if constexpr (SMEM_MATS) {
     double* sSo = mats;
-    double* sDi = mats + (size_t)N * BS;
-    const double2* gSo = reinterpret_cast<const double2*>(P.Soff + (size_t)b * N * BS);
-    for (int idx = t; idx < N * BS / 2; idx += blockDim.x) reinterpret_cast<double2*>(sSo)[idx] = gSo[idx];
+    double* sSd = sSo + (size_t)N * L::BSP;
+    double* sDi = sSd + (size_t)nb * L::TRP;
+    const double* gSo = P.Soff + (size_t)b * N * BS;
+    for (int idx = t; idx < N * (BS / 2); idx += blockDim.x) {
+      const int blk = idx / (BS / 2), w = idx % (BS / 2);
+      reinterpret_cast<double2*>(sSo + (size_t)blk * L::BSP)[w] = reinterpret_cast<const double2*>(gSo + (size_t)blk * BS)[w];
+    }
+    const double* gSd = P.Sdiag + (size_t)b * nb * BS;
     const double* gDi = P.Dinv + (size_t)b * nb * TRI;
-    for (int idx = t; idx < nb * TRI; idx += blockDim.x) sDi[idx] = gDi[idx];
+    for (int idx = t; idx < nb * TRI; idx += blockDim.x) {
+      const int blk = idx / TRI, w = idx % TRI;
+      // w -> (i, j) of the lower triangle
+      int i = 0;
+      while ((i + 1) * (i + 2) / 2 <= w) ++i;
+      const int j = w - i * (i + 1) / 2;
+      const double* Sf = gSd + (size_t)blk * BS;
+      sSd[(size_t)blk * L::TRP + w] = 0.5 * (Sf[i * NX + j] + Sf[j * NX + i]);
+      sDi[(size_t)blk * L::TRP + w] = gDi[(size_t)blk * TRI + w];
+    }
     So = sSo;
+    Sd = sSd;
     Di = sDi;
   } else {
     So = P.Soff + (size_t)b * N * BS;
+    Sd = P.Sdiag + (size_t)b * nb * BS;
     Di = P.Dinv + (size_t)b * nb * TRI;
   }
-  const bool valid = t < nb * HN;
-  const int k = valid ? t / HN : 0;
-  const int i0 = valid ? t % HN : 0, i1 = i0 + HN;
+  const bool valid = t < nb;
+  const int k = valid ? t : 0;
   BlockReducer R{red, 0, (int)((blockDim.x + 31) >> 5)};
 
-  const double* Sdk = P.Sdiag + ((size_t)b * nb + k) * BS;
-  double sd0[SD_REGS ? NX : 1], sd1[SD_REGS ? NX : 1];
-  if constexpr (SD_REGS) {
+  auto apply_S_diag = [&](const double* v, double* y) {
+    if constexpr (SMEM_MATS) sym_apply_packed<NX>(Sd + (size_t)k * SST, v, y);
+    else sym_apply_full<NX>(Sd + (size_t)k * SST, v, y);
+  };
+  auto apply_D_inv = [&](const double* v, double* y) {
+    if constexpr (SMEM_MATS) sym_apply_packed<NX>(Di + (size_t)k * DST, v, y);
+    else {
+      // packed in global memory: 8-byte loads (blocks of TRI doubles are not 16-byte aligned)
+      const double* Mp = Di + (size_t)k * DST;
+      int idx = 0;
 #pragma unroll
-    for (int j = 0; j < NX; ++j) {
-      sd0[j] = valid ? Sdk[i0 * NX + j] : 0.0;
-      sd1[j] = valid ? Sdk[i1 * NX + j] : 0.0;
+      for (int i = 0; i < NX; ++i) {
+#pragma unroll
+        for (int j = 0; j <= i; ++j, ++idx) {
+          const double m = Mp[idx];
+          if (j < i) {
+            y[i] = fma(m, v[j], y[i]);
+            y[j] = fma(m, v[i], y[j]);
+          } else {
+            y[i] = fma(m, v[i], y[i]);
+          }
+        }
+      }
+    }
+  };
+  // y += phi_{k-1} v_{k-1} + phi_k^T v_{k+1}, neighbours' vectors read from the exchange buffer
+  auto apply_off = [&](const double* buf, double* y) {
+    double vn[NX];
+    if (k > 0) {
+      vec_load<NX>(buf + (k - 1) * NX, vn);
+      off_apply_rows<NX>(So + (size_t)(k - 1) * OST, vn, y);
+    }
+    if (k < N) {
+      vec_load<NX>(buf + (k + 1) * NX, vn);
+      off_apply_cols<NX>(So + (size_t)k * OST, vn, y);
+    }
+  };
+
+  double lam[NX], r[NX], p[NX], z[NX];
+  {
+    const double* gam = P.gamma + (size_t)b * vlen + k * NX;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      lam[i] = 0.0;
+      r[i] = valid ? gam[i] : 0.0;
+      p[i] = 0.0;
     }
   }
-  const double* gam = P.gamma + (size_t)b * vlen;
-  double r0 = valid ? gam[k * NX + i0] : 0.0, r1 = valid ? gam[k * NX + i1] : 0.0;
-  double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
-
   // violation of the current iterate: |x_s - x_0|_1 + sum |e|_1  (sqp.py:111-115)
   double viol_part = 0.0;
   if (valid) {
     if (k < N) {
       const double* eb = P.e + ((size_t)b * N + k) * NX;
-      viol_part = fabs(eb[i0]) + fabs(eb[i1]);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) viol_part += fabs(eb[i]);
     }
     if (k == 0) {
       const double* xs = P.x_start + (size_t)b * NX;
       const double* x0 = P.X + (size_t)b * nb * NX;
-      viol_part += fabs(xs[i0] - x0[i0]) + fabs(xs[i1] - x0[i1]);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) viol_part += fabs(xs[i] - x0[i]);
     }
   }
-
-  // off-diagonal product rows (k,i0),(k,i1) of  phi_{k-1} v_{k-1} + phi_k^T v_{k+1}
-  auto offmv = [&](const double* v, double& y0, double& y1) {
-    y0 = 0.0;
-    y1 = 0.0;
-    if (k > 0) {
-      const double* O = So + (size_t)(k - 1) * BS;
-      const double* vm = v + (k - 1) * NX;
-      y0 = dot_row<NX>(O + i0 * NX, vm);
-      y1 = dot_row<NX>(O + i1 * NX, vm);
-    }
-    if (k < N) {
-      const double* O = So + (size_t)k * BS;
-      const double* vn = v + (k + 1) * NX;
-      double s0 = 0.0, s1 = 0.0;
+  auto dot = [&](const double* a, const double* c) {
+    double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < NX; ++j) {
-        s0 = fma(O[j * NX + i0], vn[j], s0);
-        s1 = fma(O[j * NX + i1], vn[j], s1);
-      }
-      y0 += s0;
-      y1 += s1;
-    }
+    for (int i = 0; i < NX; ++i) acc = fma(a[i], c[i], acc);
+    return acc;
   };
-  auto dinv_apply = [&](const double* v, double& y0, double& y1) {
-    const double* D = Di + (size_t)k * TRI;
-    const double* vk = v + k * NX;
-    const int base0 = i0 * (i0 + 1) / 2, base1 = i1 * (i1 + 1) / 2;
-    double a0 = 0.0, a1 = 0.0;
+  // z = Phi^-1 r (thread-private result); one barrier
+  auto precondition = [&]() {
+    double w[NX];
 #pragma unroll
-    for (int j = 0; j < NX; ++j) {
-      const int tj = j * (j + 1) / 2;
-      const double vj = vk[j];
-      a0 = fma(D[(j <= i0) ? base0 + j : tj + i0], vj, a0);
-      a1 = fma(D[(j <= i1) ? base1 + j : tj + i1], vj, a1);
-    }
-    y0 = a0;
-    y1 = a1;
-  };
-  // z = Phi^-1 r for the current (r0, r1); uses vr, vw; result thread-private
-  auto precondition = [&](double& z0, double& z1) {
+    for (int i = 0; i < NX; ++i) w[i] = 0.0;
     if (valid) {
-      vr[k * NX + i0] = r0;
-      vr[k * NX + i1] = r1;
+      apply_D_inv(r, w);
+      vec_store<NX>(vA + k * NX, w);
     }
     __syncthreads();
-    double w0 = 0.0, w1 = 0.0;
-    if (valid) {
-      dinv_apply(vr, w0, w1);
-      vw[k * NX + i0] = w0;
-      vw[k * NX + i1] = w1;
+    double u[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      u[i] = 0.0;
+      z[i] = 0.0;
     }
-    __syncthreads();
-    double t0 = 0.0, t1 = 0.0;
     if (valid) {
-      offmv(vw, t0, t1);  // every read of vr (dinv_apply above) precedes the barrier just passed
-      vr[k * NX + i0] = r0 - t0;
-      vr[k * NX + i1] = r1 - t1;
+      apply_off(vA, u);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) u[i] = r[i] - u[i];
+      apply_D_inv(u, z);
     }
-    __syncthreads();
-    if (valid) dinv_apply(vr, z0, z1);
-    else z0 = z1 = 0.0;
   };
 
   int its = 0, breakdown = 0;
   bool nan_curv = false;
-  double2 s = R.sum2(r0 * r0 + r1 * r1, viol_part);
+  double2 s = R.sum2(dot(r, r), viol_part);   // (also orders the shared-memory fill before first use)
   double res = sqrt(s.x);
   const double viol = s.y;
   if (!(res <= P.pcg_tol)) {
-    double z0, z1;
-    precondition(z0, z1);
-    p0 = z0;
-    p1 = z1;
-    double rz = R.sum2(r0 * z0 + r1 * z1, 0.0).x;
+    precondition();
+#pragma unroll
+    for (int i = 0; i < NX; ++i) p[i] = z[i];
+    double rz = R.sum2(dot(r, z), 0.0).x;
     const int cap = P.pcg_cap;
     for (int it = 1; it <= cap; ++it) {
-      if (valid) {
-        vp[k * NX + i0] = p0;
-        vp[k * NX + i1] = p1;
-      }
+      if (valid) vec_store<NX>(vB + k * NX, p);
       __syncthreads();
-      double q0 = 0.0, q1 = 0.0;
-      if (valid) {
-        const double* vk = vp + k * NX;
-        double a0 = 0.0, a1 = 0.0;
-        if constexpr (SD_REGS) {
+      double q[NX];
 #pragma unroll
-          for (int j = 0; j < NX; ++j) {
-            a0 = fma(sd0[j], vk[j], a0);
-            a1 = fma(sd1[j], vk[j], a1);
-          }
-        } else {
-          a0 = dot_row<NX>(Sdk + i0 * NX, vk);
-          a1 = dot_row<NX>(Sdk + i1 * NX, vk);
-        }
-        double o0, o1;
-        offmv(vp, o0, o1);
-        q0 = a0 + o0;
-        q1 = a1 + o1;
+      for (int i = 0; i < NX; ++i) q[i] = 0.0;
+      if (valid) {
+        apply_S_diag(p, q);
+        apply_off(vB, q);
       }
-      const double curv = R.sum2(p0 * q0 + p1 * q1, 0.0).x;
+      const double curv = R.sum2(dot(p, q), 0.0).x;
       if (curv <= 0.0) {  // blocktri.py:158-161
         breakdown = it;
         break;
@@ -762,23 +884,26 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg(SolveParams P) {
         break;
       }
       const double a = rz / curv;
-      l0 = l0 + a * p0;
-      l1 = l1 + a * p1;
-      r0 = r0 - a * q0;
-      r1 = r1 - a * q1;
-      double z0n, z1n;
-      precondition(z0n, z1n);
-      const double2 rr = R.sum2(r0 * z0n + r1 * z1n, r0 * r0 + r1 * r1);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) {
+        lam[i] = lam[i] + a * p[i];
+        r[i] = r[i] - a * q[i];
+      }
+      precondition();
+      const double2 rr = R.sum2(dot(r, z), dot(r, r));
       res = sqrt(rr.y);
       its = it;
       if (res <= P.pcg_tol) break;
       const double beta = rr.x / rz;
-      p0 = z0n + beta * p0;
-      p1 = z1n + beta * p1;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) p[i] = z[i] + beta * p[i];
       rz = rr.x;
     }
   }
-  if (nan_curv) l0 = l1 = nan("");
+  if (nan_curv) {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) lam[i] = nan("");
+  }
 
   if (breakdown) {
     if (t == 0) {
@@ -794,66 +919,54 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg(SolveParams P) {
     return;
   }
 
-  // ---- recover_step (qpform.py:375-397) ----
+  // ---- recover_step (qpform.py:375-397).  -Q^-1 A_k^T lam_{k+1} = phi_k^T lam_{k+1} reuses the
+  // resident sub-diagonal blocks instead of re-reading A_k from global memory. ----
   __syncthreads();
-  double* vl = vp;  // lambda
-  double* vg = vr;  // grad_x
-  double* vu = vw;  // grad_u  [N][NU]
   if (valid) {
-    vl[k * NX + i0] = l0;
-    vl[k * NX + i1] = l1;
-    P.lam[(size_t)b * vlen + k * NX + i0] = l0;
-    P.lam[(size_t)b * vlen + k * NX + i1] = l1;
+    vec_store<NX>(vA + k * NX, lam);
+    double* lg = P.lam + (size_t)b * vlen + k * NX;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) lg[i] = lam[i];
   }
   __syncthreads();
   const double* hinv = P.hinv + (size_t)b * HS;
-  if (valid) {
-    const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
-    double g0 = g[i0] - l0, g1 = g[i1] - l1;
-    if (k < N) {
-      const double* Ak = P.A + ((size_t)b * N + k) * BS;
-      const double* ln = vl + (k + 1) * NX;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int j = 0; j < NX; ++j) {
-        s0 = fma(Ak[j * NX + i0], ln[j], s0);
-        s1 = fma(Ak[j * NX + i1], ln[j], s1);
-      }
-      g0 += s0;
-      g1 += s1;
-      const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
-      for (int ju = i0; ju < NU; ju += HN) {
-        double su = 0.0;
-#pragma unroll
-        for (int j = 0; j < NX; ++j) su = fma(Bk[j * NU + ju], ln[j], su);
-        vu[k * NU + ju] = g[NX + ju] + su;
-      }
-    }
-    vg[k * NX + i0] = g0;
-    vg[k * NX + i1] = g1;
-  }
-  __syncthreads();
   double step_part = 0.0;
   if (valid) {
+    const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
+    double gx[NX], dx[NX], ln[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) gx[i] = g[i] - lam[i];
     const double* Qk = (k < N) ? hinv : hinv + BS;
-    const double* gk = vg + k * NX;
-    const double d0 = -dot_row<NX>(Qk + i0 * NX, gk);
-    const double d1 = -dot_row<NX>(Qk + i1 * NX, gk);
-    double* dX = P.dX + ((size_t)b * nb + k) * NX;
-    dX[i0] = d0;
-    dX[i1] = d1;
-    step_part = nanmax(fabs(d0), fabs(d1));
+#pragma unroll
+    for (int i = 0; i < NX; ++i) dx[i] = -dot_row<NX>(Qk + i * NX, gx);
     if (k < N) {
+      vec_load<NX>(vA + (k + 1) * NX, ln);
+      off_apply_cols<NX>(So + (size_t)k * OST, ln, dx);
+      const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
       const double* Ri = hinv + 2 * BS;
-      const double* gu = vu + k * NU;
+      double gu[NU];
+#pragma unroll
+      for (int ju = 0; ju < NU; ++ju) gu[ju] = g[NX + ju];
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+#pragma unroll
+        for (int ju = 0; ju < NU; ++ju) gu[ju] = fma(Bk[j * NU + ju], ln[j], gu[ju]);
+      }
       double* dU = P.dU + ((size_t)b * N + k) * NU;
-      for (int ju = i0; ju < NU; ju += HN) {
+#pragma unroll
+      for (int ju = 0; ju < NU; ++ju) {
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
         dU[ju] = -acc;
         step_part = nanmax(step_part, fabs(acc));
       }
+    }
+    double* dX = P.dX + ((size_t)b * nb + k) * NX;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      dX[i] = dx[i];
+      step_part = nanmax(step_part, fabs(dx[i]));
     }
   }
   const double step_inf = R.max1(step_part);
