@@ -5,8 +5,8 @@
 namespace gato {
 
 // -----------------------------------------------------------------------------------------
-// k_init: per-solve state (sqp.py:222-229).  merit_current is filled by a line-search pass
-// at alpha = 0 followed by k_init_merit.
+// k_init: per-solve state (sqp.py:222-229).  merit_current is filled by the first pass: its line
+// search carries an extra alpha = 0 candidate (k_linesearch) that k_update reads.
 // -----------------------------------------------------------------------------------------
 __global__ void k_init(SolveParams P) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -35,12 +35,6 @@ __global__ void k_init(SolveParams P) {
   info[GATO_INFO_FAIL_KNOT] = -1;
 }
 
-__global__ void k_init_merit(SolveParams P) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= P.M) return;
-  P.sd[b * SD_WORDS + SD_MERIT] = P.merits[(size_t)b * P.C];
-  P.si[b * SI_WORDS + SI_MERIT_VALID] = 1;
-}
 
 // -----------------------------------------------------------------------------------------
 // k_update: per solve: first-minimum argmin over the candidates, strict-decrease accept test
@@ -56,9 +50,22 @@ __global__ void __launch_bounds__(128) k_update(SolveParams P, int nx, int nu, c
   __shared__ int s_accept;
   const int active = si[SI_ACTIVE];
   const int skip = si[SI_SKIP_LS];
+  if (skip == 2) {   // tolerance exit at the very first iteration: patch merit(X0, U0) into its record
+    if (threadIdx.x == 0) {
+      const double m0 = P.merits[(size_t)b * (P.C + 1) + P.C];
+      P.sd[b * SD_WORDS + SD_MERIT] = m0;
+      P.trace[((size_t)b * P.max_it + si[SI_IT]) * GATO_TRACE_WORDS + GATO_TRACE_MERIT] = m0;
+      si[SI_MERIT_VALID] = 1;
+      si[SI_SKIP_LS] = 1;
+    }
+  }
   if (active && !skip) {
     if (threadIdx.x == 0) {
-      const double* mer = P.merits + (size_t)b * P.C;
+      const double* mer = P.merits + (size_t)b * (P.C + 1);
+      if (!si[SI_MERIT_VALID]) {
+        P.sd[b * SD_WORDS + SD_MERIT] = mer[P.C];
+        si[SI_MERIT_VALID] = 1;
+      }
       int best = 0;
       double bm = mer[0];
       for (int c = 1; c < P.C; ++c)
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(128) k_update(SolveParams P, int nx, int nu, c
       double merit = cur;
       if (accepted) {
         merit = bm;
-        viol = P.viols[(size_t)b * P.C + best];
+        viol = P.viols[(size_t)b * (P.C + 1) + best];
         P.sd[b * SD_WORDS + SD_MERIT] = bm;
       }
       const int it = si[SI_IT];

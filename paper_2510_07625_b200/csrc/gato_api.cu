@@ -63,6 +63,8 @@ struct gato_handle {
   cudaGraphConditionalHandle cond = 0;
   bool graph_valid = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t side = nullptr;             // k_hessinv branch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t launches = 0;
   void* lin_scratch = nullptr;  // model-private linearisation scratch (iiwa14: per-stage link data)
 };
@@ -91,20 +93,31 @@ int dev_alloc(gato_handle* h, const char* name, T** out, int64_t count) {
 }
 
 // one SQP pass: six launches
+// One SQP pass.  k_hessinv only depends on the previous pass, so it runs on the side stream
+// concurrently with the linearisation (a parallel branch once captured into the graph).
 // `marks`, when given, receives one event before each of the six launches and one after the last
+// (everything serial on `s`, for per-kernel timing).
 int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond, cudaEvent_t* marks = nullptr) {
   const SolveParams& P = h->P;
   RowView V{P.X, P.U, P.force, P.N, P.si};
-  if (marks) CK(cudaEventRecord(marks[0], s));
-  CK(h->ops.hessinv(P, s));
-  if (marks) CK(cudaEventRecord(marks[1], s));
+  if (marks) {
+    CK(cudaEventRecord(marks[0], s));
+    CK(h->ops.hessinv(P, s));
+    CK(cudaEventRecord(marks[1], s));
+  } else {
+    CK(cudaEventRecord(h->ev_fork, s));
+    CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    CK(h->ops.hessinv(P, h->side));
+    CK(cudaEventRecord(h->ev_join, h->side));
+  }
   CK(h->ops.linearize(V, P.mp, P.h, (int64_t)P.M * P.N, P.A, P.B, P.e, h->lin_scratch, s));
   if (marks) CK(cudaEventRecord(marks[2], s));
+  else CK(cudaStreamWaitEvent(s, h->ev_join, 0));
   CK(h->ops.schur(P, s));
   if (marks) CK(cudaEventRecord(marks[3], s));
   CK(h->ops.pcg(P, s));
   if (marks) CK(cudaEventRecord(marks[4], s));
-  CK(h->ops.linesearch(P, 0, s));
+  CK(h->ops.linesearch(P, s));
   if (marks) CK(cudaEventRecord(marks[5], s));
   k_update<<<P.M, 128, 0, s>>>(P, h->ops.nx, h->ops.nu, h->cond, use_cond);
   CK(cudaGetLastError());
@@ -115,9 +128,6 @@ int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond, cudaEvent_t* mark
 int enqueue_prologue(gato_handle* h, cudaStream_t s) {
   const SolveParams& P = h->P;
   k_init<<<(P.M + 127) / 128, 128, 0, s>>>(P);
-  CK(cudaGetLastError());
-  CK(h->ops.linesearch(P, 1, s));
-  k_init_merit<<<(P.M + 127) / 128, 128, 0, s>>>(P);
   CK(cudaGetLastError());
   return GATO_OK;
 }
@@ -244,12 +254,13 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   ALLOC(Sdiag, M * nb * nx * nx);
   ALLOC(Soff, M * N * nx * nx);
   ALLOC(Dinv, M * nb * (nx * (nx + 1) / 2));
+  ALLOC(pmats, M * (int64_t)h->ops.pcg_mat_doubles((int)N));
   ALLOC(gamma, M * nb * nx);
   ALLOC(lam, M * nb * nx);
   ALLOC(dX, M * nb * nx);
   ALLOC(dU, M * N * nu);
-  ALLOC(merits, M * P.C);
-  ALLOC(viols, M * P.C);
+  ALLOC(merits, M * (P.C + 1));
+  ALLOC(viols, M * (P.C + 1));
   ALLOC(alphas, P.C);
   ALLOC(sd, M * SD_WORDS);
   ALLOC(si, M * SI_WORDS);
@@ -272,6 +283,9 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   CK(cudaMemcpy(P.alphas, alphas.data(), P.C * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaEventCreate(&h->ev0));
   CK(cudaEventCreate(&h->ev1));
+  CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CK(h->ops.prepare(P));
   h->loop_mode = cfg->loop_mode ? cfg->loop_mode : env_int("GATO_LOOP_MODE", 1);
   return GATO_OK;
@@ -407,7 +421,7 @@ int64_t gato_launch_count(const gato_handle* h) {
   if (!h) return 0;
   unsigned int c[4] = {0, 0, 0, 0};
   if (cudaMemcpy(c, h->P.counters, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return 3 + 6 * (int64_t)c[3];
+  return 1 + 6 * (int64_t)c[3];
 }
 
 int gato_loop_mode(const gato_handle* h) { return h ? h->loop_mode : 0; }
@@ -491,6 +505,9 @@ void gato_destroy(gato_handle* h) {
   destroy_graph(h);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->side) cudaStreamDestroy(h->side);
   for (void* p : h->allocs) cudaFree(p);
   delete h;
 }

@@ -18,9 +18,10 @@ struct ModelOps {
   size_t (*lin_scratch_bytes)(int64_t rows);
   cudaError_t (*schur)(const SolveParams&, cudaStream_t);
   cudaError_t (*pcg)(const SolveParams&, cudaStream_t);
-  cudaError_t (*linesearch)(const SolveParams&, int, cudaStream_t);
+  cudaError_t (*linesearch)(const SolveParams&, cudaStream_t);
   cudaError_t (*step_rows)(const ModelParams&, double, int64_t, const double*, const double*, const double*,
                            double*, cudaStream_t);
+  size_t (*pcg_mat_doubles)(int N);            // per-solve padded matrix record (PcgLayout)
   cudaError_t (*prepare)(const SolveParams&);  // opt-in shared memory sizes, outside any capture
 };
 
@@ -87,11 +88,11 @@ cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
 }
 
 template <class Mdl>
-cudaError_t launch_linesearch(const SolveParams& P, int init, cudaStream_t s) {
+cudaError_t launch_linesearch(const SolveParams& P, cudaStream_t s) {
   int threads = ((P.N + 31) / 32) * 32;
   if (threads > 128) threads = 128;
-  dim3 grid(init ? 1 : P.C, P.M);
-  k_linesearch<Mdl><<<grid, threads, 0, s>>>(P, init);
+  dim3 grid(P.C + 1, P.M);   // C step-length candidates + the alpha = 0 candidate of the first iteration
+  k_linesearch<Mdl><<<grid, threads, 0, s>>>(P);
   return cudaGetLastError();
 }
 
@@ -101,6 +102,11 @@ cudaError_t launch_step_rows(const ModelParams& mp, double h, int64_t rows, cons
   const int threads = 64;
   k_step_rows<Mdl><<<(unsigned)((rows + threads - 1) / threads), threads, 0, s>>>(mp, h, rows, X, U, F, out);
   return cudaGetLastError();
+}
+
+template <class Mdl>
+size_t pcg_mat_doubles(int N) {
+  return PcgLayout<Mdl::NX>::mat_doubles(N);
 }
 
 template <class Mdl>
@@ -124,7 +130,7 @@ template <class Mdl>
 ModelOps make_ops() {
   return ModelOps{Mdl::NX,           Mdl::NU,           Mdl::NF,
                   launch_hessinv<Mdl>, launch_linearize<Mdl>, lin_scratch_bytes<Mdl>, launch_schur<Mdl>,
-                  launch_pcg<Mdl>,     launch_linesearch<Mdl>, launch_step_rows<Mdl>, prepare_attrs<Mdl>};
+                  launch_pcg<Mdl>,     launch_linesearch<Mdl>, launch_step_rows<Mdl>, pcg_mat_doubles<Mdl>, prepare_attrs<Mdl>};
 }
 
 

@@ -39,7 +39,7 @@ struct SolveParams {
   double *X, *U, *trace;
   int32_t* info;
   // scratch
-  double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Dinv, *gamma, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
+  double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Dinv, *pmats, *gamma, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
   int32_t *si, *pcg_iters;
   unsigned int* counters;  // [0] active count, [1] ticket, [2] pending solves, [3] passes run
 };
@@ -57,49 +57,72 @@ __device__ __forceinline__ int tri_idx(int i, int j) { return i >= j ? i * (i + 
 // W: D*D row-major in shared memory (in: matrix, out: inverse), T: D*D scratch.
 // -----------------------------------------------------------------------------------------
 template <int D>
-__device__ __forceinline__ int warp_spd_inverse(double* W, double* T, int lane) {
+struct SpdScratch {
+  double L[D * (D + 1)];      // factor, row stride D + 1 (odd for even D: conflict-free rows)
+  double invd[D + (D & 1)];   // reciprocals of the factor's diagonal
+};
+
+template <int D>
+__device__ __forceinline__ int warp_spd_inverse(double* W, SpdScratch<D>& S, int lane) {
+  constexpr int LD = D + 1;
+  for (int idx = lane; idx < D * D; idx += 32) S.L[(idx / D) * LD + idx % D] = W[idx];
+  __syncwarp();
   int fail = 0;
   for (int j = 0; j < D; ++j) {
-    const double d = W[j * D + j];
-    if (!(d > 0.0)) {
+    const double d = S.L[j * LD + j];
+    if (!(d > 0.0)) {   // dpotrf: pivot <= 0 or NaN
       fail = j + 1;
       break;
     }
-    const double r = sqrt(d);
+    const double r = sqrt(d), ir = 1.0 / r;
     __syncwarp();
-    if (lane == j) W[j * D + j] = r;
-    if (lane > j && lane < D) W[lane * D + j] = W[lane * D + j] / r;
+    if (lane == j) {
+      S.L[j * LD + j] = r;
+      S.invd[j] = ir;
+    }
+    if (lane > j && lane < D) S.L[lane * LD + j] = S.L[lane * LD + j] * ir;
     __syncwarp();
-    if (lane > j && lane < D) {
-      const double lij = W[lane * D + j];
-      for (int k = j + 1; k <= lane; ++k) W[lane * D + k] = fma(-lij, W[k * D + j], W[lane * D + k]);
+    // trailing update of the lower triangle, (i, k) pairs spread over the 32 lanes
+    const int rem = D - j - 1;
+    for (int pidx = lane; pidx < rem * (rem + 1) / 2; pidx += 32) {
+      int ii = (int)((sqrtf(8.0f * pidx + 1.0f) - 1.0f) * 0.5f);
+      while ((ii + 1) * (ii + 2) / 2 <= pidx) ++ii;
+      while (ii * (ii + 1) / 2 > pidx) --ii;
+      const int kk = pidx - ii * (ii + 1) / 2;
+      const int i = j + 1 + ii, k = j + 1 + kk;
+      S.L[i * LD + k] = fma(-S.L[i * LD + j], S.L[k * LD + j], S.L[i * LD + k]);
     }
     __syncwarp();
   }
   if (fail) return fail;
-  if (lane < D) {
+  if (lane < D) {   // column `lane` of the inverse: L y = e, L^T x = y
     double y[D];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       double t = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
-      for (int k = 0; k < i; ++k) t = fma(-W[i * D + k], y[k], t);
-      y[i] = t / W[i * D + i];
+      for (int k = 0; k < i; ++k) t = fma(-S.L[i * LD + k], y[k], t);
+      y[i] = t * S.invd[i];
     }
 #pragma unroll
     for (int i = D - 1; i >= 0; --i) {
       double t = y[i];
 #pragma unroll
-      for (int k = i + 1; k < D; ++k) t = fma(-W[k * D + i], y[k], t);
-      y[i] = t / W[i * D + i];
+      for (int k = i + 1; k < D; ++k) t = fma(-S.L[k * LD + i], y[k], t);
+      y[i] = t * S.invd[i];
     }
 #pragma unroll
-    for (int i = 0; i < D; ++i) T[i * D + lane] = y[i];
+    for (int i = 0; i < D; ++i) W[i * D + lane] = y[i];
   }
   __syncwarp();
-  for (int idx = lane; idx < D * D; idx += 32) {
-    const int i = idx / D, j = idx % D;
-    W[idx] = 0.5 * (T[i * D + j] + T[j * D + i]);
+  for (int pidx = lane; pidx < D * (D - 1) / 2; pidx += 32) {   // symmetrise in place, pairs i > j
+    int i = (int)((sqrtf(8.0f * pidx + 1.0f) - 1.0f) * 0.5f);
+    while ((i + 1) * (i + 2) / 2 <= pidx) ++i;
+    while (i * (i + 1) / 2 > pidx) --i;
+    const int j = pidx - i * (i + 1) / 2;
+    const double m = 0.5 * (W[(i + 1) * D + j] + W[j * D + i + 1]);
+    W[(i + 1) * D + j] = m;
+    W[j * D + i + 1] = m;
   }
   __syncwarp();
   return 0;
@@ -127,7 +150,9 @@ template <int NX, int NU>
 __global__ void __launch_bounds__(96) k_hessinv(SolveParams P) {
   const int b = blockIdx.x;
   if (!P.si[b * SI_WORDS + SI_ACTIVE]) return;
-  __shared__ double W[3][NX * NX], T[3][NX * NX];
+  __shared__ double W[3][NX * NX];
+  __shared__ SpdScratch<NX> scr[2];
+  __shared__ SpdScratch<NU> scr_u;
   __shared__ int fails[3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double rho = P.sd[b * SD_WORDS + SD_RHO];
@@ -137,14 +162,14 @@ __global__ void __launch_bounds__(96) k_hessinv(SolveParams P) {
     const double* src = (warp == 0 ? P.Q : P.QN) + (size_t)b * NX * NX;
     for (int idx = lane; idx < NX * NX; idx += 32) W[warp][idx] = src[idx] + ((idx / NX == idx % NX) ? rho : 0.0);
     __syncwarp();
-    fails[warp] = warp_spd_inverse<NX>(W[warp], T[warp], lane);
+    fails[warp] = warp_spd_inverse<NX>(W[warp], scr[warp], lane);
     for (int idx = lane; idx < NX * NX; idx += 32) out[warp * NX * NX + idx] = W[warp][idx];
   } else {
     const double* src = P.R + (size_t)b * NU * NU;
     const double rr = P.regularize_r ? rho : 0.0;
     for (int idx = lane; idx < NU * NU; idx += 32) W[2][idx] = src[idx] + ((idx / NU == idx % NU) ? rr : 0.0);
     __syncwarp();
-    fails[2] = warp_spd_inverse<NU>(W[2], T[2], lane);
+    fails[2] = warp_spd_inverse<NU>(W[2], scr_u, lane);
     for (int idx = lane; idx < NU * NU; idx += 32) out[2 * NX * NX + idx] = W[2][idx];
   }
   __syncthreads();
@@ -358,6 +383,25 @@ __global__ void k_step_rows(ModelParams mp, double h, int64_t rows, const double
   for (int i = 0; i < NX; ++i) out[r * NX + i] = o[i];
 }
 
+// smallest even m >= n with m / 2 odd: a block stride of m doubles puts consecutive lanes on
+// distinct 16-byte bank groups for 128-bit shared-memory loads
+__host__ __device__ constexpr int pad_stride(int n) {
+  int m = (n + 1) & ~1;
+  return ((m / 2) % 2 == 0) ? m + 2 : m;
+}
+
+template <int NX>
+struct PcgLayout {
+  static constexpr int BS = NX * NX, TRI = NX * (NX + 1) / 2;
+  static constexpr int BSP = pad_stride(BS), TRP = pad_stride(TRI);
+  static constexpr int VSTRIDE = NX;   // exchange vectors: NX doubles per block row (NX even)
+  __host__ __device__ static size_t vec_bytes(int nb) { return 2 * (size_t)(nb * NX + 2) * 8 + 64 * 16; }
+  // per-solve matrix record, identical in global scratch (pmats) and in shared memory:
+  //   [ phi_0 .. phi_{N-1}  (BSP each) | packed S_00 .. S_NN (TRP each) | packed D_0^-1 .. D_N^-1 (TRP each) ]
+  __host__ __device__ static size_t mat_doubles(int N) { return (size_t)N * BSP + 2 * (size_t)(N + 1) * TRP; }
+  __host__ __device__ static size_t mat_bytes(int N) { return mat_doubles(N) * 8; }
+};
+
 // -----------------------------------------------------------------------------------------
 // k_schur: one warp per block row k of one solve (form_schur qpform.py:290-339 and the
 // diagonal part of form_preconditioner qpform.py:342-353):
@@ -367,16 +411,24 @@ __global__ void k_step_rows(ModelParams mp, double h, int64_t rows, const double
 // The stair preconditioner's off-diagonal blocks -D_{k+1}^-1 phi_k D_k^-1 (qpform.py:355-356)
 // are never formed: k_pcg applies Phi^-1 in factored form, which needs no neighbour's D^-1
 // here and therefore no grid-wide synchronisation.
+// Lane (r, half) computes a 1 x NX/2 strip of every product, with A^T and B^T staged so that
+// every shared-memory read is a row read.  Besides the plain arrays (Sdiag, Soff, Dinv: parity
+// tests, step recovery) the warp writes its part of the padded per-solve matrix record that
+// k_pcg pulls into shared memory with one bulk copy.
 // -----------------------------------------------------------------------------------------
 template <int NX, int NU>
 struct SchurSmem {
-  double A[NX * NX], B[NX * NU], AQ[NX * NX], BR[NX * NU], W[NX * NX], T[NX * NX];
-  double qk[NX], qj[NX], rj[NU], dxk[NX], dxj[NX];
+  double A[NX * NX], AT[NX * NX], B[NX * NU], BT[NU * NX], Q[NX * NX], R[NU * NU + (NU & 1)];
+  double AQ[NX * NX], BR[NX * NU], W[NX * NX];
+  SpdScratch<NX> spd;
+  double qk[NX], qj[NX], rj[NU + (NU & 1)], dxk[NX], dxj[NX];
 };
 
 template <int NX, int NU, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_schur(SolveParams P) {
-  extern __shared__ double schur_smem_raw[];
+__global__ void __launch_bounds__(WARPS * 32, 4) k_schur(SolveParams P) {
+  extern __shared__ __align__(16) double schur_smem_raw[];
+  using L = PcgLayout<NX>;
+  constexpr int HALF = NX / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t wg = (int64_t)blockIdx.x * WARPS + warp;
   const int nb = P.N + 1;
@@ -395,6 +447,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_schur(SolveParams P) {
   const double* QNw = P.QN + (size_t)b * NX * NX;
   const double* Rw = P.R + (size_t)b * NU * NU;
   double* grad = P.grad + ((size_t)b * nb + k) * (NX + NU);
+  double* pm = P.pmats + (size_t)b * L::mat_doubles(P.N);
 
   // gradients with the undamped weights (qpform.py:185-186,195)
   if (lane < NX) {
@@ -452,37 +505,77 @@ __global__ void __launch_bounds__(WARPS * 32) k_schur(SolveParams P) {
     const int j = k - 1;
     const double* Ag = P.A + ((size_t)b * P.N + j) * NX * NX;
     const double* Bg = P.B + ((size_t)b * P.N + j) * NX * NU;
-    for (int idx = lane; idx < NX * NX; idx += 32) S.A[idx] = Ag[idx];
-    for (int idx = lane; idx < NX * NU; idx += 32) S.B[idx] = Bg[idx];
-    __syncwarp();
     for (int idx = lane; idx < NX * NX; idx += 32) {
-      const int r = idx / NX, c = idx % NX;
-      double acc = 0.0;
-#pragma unroll
-      for (int l = 0; l < NX; ++l) acc = fma(S.A[r * NX + l], Qi[l * NX + c], acc);
-      S.AQ[idx] = acc;
+      const double v = Ag[idx];
+      S.A[idx] = v;
+      S.AT[(idx % NX) * NX + idx / NX] = v;
+      S.Q[idx] = Qi[idx];
     }
     for (int idx = lane; idx < NX * NU; idx += 32) {
-      const int r = idx / NU, c = idx % NU;
-      double acc = 0.0;
+      const double v = Bg[idx];
+      S.B[idx] = v;
+      S.BT[(idx % NU) * NX + idx / NU] = v;
+    }
+    for (int idx = lane; idx < NU * NU; idx += 32) S.R[idx] = Ri[idx];
+    __syncwarp();
+    const int r = lane >> 1, c0 = (lane & 1) * HALF;
+    const bool strip = lane < 2 * NX;
+    if (strip) {   // AQ[r][c0 .. c0+HALF) = A[r][:] Q^-1[:, c0 ..]
+      double acc[HALF];
 #pragma unroll
-      for (int l = 0; l < NU; ++l) acc = fma(S.B[r * NU + l], Ri[l * NU + c], acc);
-      S.BR[idx] = acc;
+      for (int i = 0; i < HALF; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int l = 0; l < NX; ++l) {
+        const double a = S.A[r * NX + l];
+#pragma unroll
+        for (int i = 0; i < HALF; ++i) acc[i] = fma(a, S.Q[l * NX + c0 + i], acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < HALF; ++i) S.AQ[r * NX + c0 + i] = acc[i];
+    }
+    if (lane < NX) {   // BR[lane][:] = B[lane][:] R^-1
+      double acc[NU];
+#pragma unroll
+      for (int i = 0; i < NU; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int l = 0; l < NU; ++l) {
+        const double bv = S.B[lane * NU + l];
+#pragma unroll
+        for (int i = 0; i < NU; ++i) acc[i] = fma(bv, S.R[l * NU + i], acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < NU; ++i) S.BR[lane * NU + i] = acc[i];
     }
     __syncwarp();
     const double* Qk = (k < P.N) ? Qi : Qti;
     double* So = P.Soff + ((size_t)b * P.N + j) * NX * NX;
-    for (int idx = lane; idx < NX * NX; idx += 32) {
-      const int r = idx / NX, c = idx % NX;
-      double t1 = 0.0, t2 = 0.0;
+    double* SoP = pm + (size_t)j * L::BSP;
+    if (strip) {   // theta[r][c0 ..] = AQ[r][:] A^T[:, c0 ..] + BR[r][:] B^T[:, c0 ..] + Qk^-1[r][c0 ..]
+      double t1[HALF], t2[HALF];
 #pragma unroll
-      for (int l = 0; l < NX; ++l) t1 = fma(S.AQ[r * NX + l], S.A[c * NX + l], t1);
+      for (int i = 0; i < HALF; ++i) t1[i] = t2[i] = 0.0;
 #pragma unroll
-      for (int l = 0; l < NU; ++l) t2 = fma(S.BR[r * NU + l], S.B[c * NU + l], t2);
-      const double th = (t1 + t2) + Qk[idx];
-      S.W[idx] = th;
-      Sd[idx] = th;
-      So[idx] = -S.AQ[idx];
+      for (int l = 0; l < NX; ++l) {
+        const double a = S.AQ[r * NX + l];
+#pragma unroll
+        for (int i = 0; i < HALF; ++i) t1[i] = fma(a, S.AT[l * NX + c0 + i], t1[i]);
+      }
+#pragma unroll
+      for (int l = 0; l < NU; ++l) {
+        const double bv = S.BR[r * NU + l];
+#pragma unroll
+        for (int i = 0; i < HALF; ++i) t2[i] = fma(bv, S.BT[l * NX + c0 + i], t2[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < HALF; ++i) {
+        const int idx = r * NX + c0 + i;
+        const double th = (t1[i] + t2[i]) + Qk[idx];
+        S.W[idx] = th;
+        Sd[idx] = th;
+        const double ph = -S.AQ[idx];
+        So[idx] = ph;
+        SoP[idx] = ph;
+      }
     }
     if (lane < NX) {
       double z1 = 0.0, z2 = 0.0, z3 = 0.0;
@@ -497,15 +590,27 @@ __global__ void __launch_bounds__(WARPS * 32) k_schur(SolveParams P) {
     }
   }
   __syncwarp();
-  const int fail = warp_spd_inverse<NX>(S.W, S.T, lane);
+  // packed symmetric copy of S_kk for the matvec (average of the two rounding-level different halves)
+  double* SdP = pm + (size_t)P.N * L::BSP + (size_t)k * L::TRP;
+  for (int idx = lane; idx < NX * NX; idx += 32) {
+    const int rr = idx / NX, cc = idx % NX;
+    if (cc <= rr) SdP[rr * (rr + 1) / 2 + cc] = 0.5 * (S.W[rr * NX + cc] + S.W[cc * NX + rr]);
+  }
+  __syncwarp();
+  const int fail = warp_spd_inverse<NX>(S.W, S.spd, lane);
   if (fail) {
     if (lane == 0) atomicMin(&P.si[b * SI_WORDS + SI_SCHUR_FAIL], k * 64 + fail);
     return;
   }
   double* Dk = P.Dinv + ((size_t)b * nb + k) * TRI;
+  double* DkP = SdP + (size_t)nb * L::TRP;
   for (int idx = lane; idx < NX * NX; idx += 32) {
-    const int r = idx / NX, c = idx % NX;
-    if (c <= r) Dk[r * (r + 1) / 2 + c] = S.W[idx];
+    const int rr = idx / NX, cc = idx % NX;
+    if (cc <= rr) {
+      const double v = S.W[idx];
+      Dk[rr * (rr + 1) / 2 + cc] = v;
+      DkP[rr * (rr + 1) / 2 + cc] = v;
+    }
   }
 }
 
@@ -588,24 +693,6 @@ struct BlockReducer {
   }
 };
 
-// smallest even m >= n with m / 2 odd: a block stride of m doubles puts consecutive lanes on
-// distinct 16-byte bank groups for 128-bit shared-memory loads
-__host__ __device__ constexpr int pad_stride(int n) {
-  int m = (n + 1) & ~1;
-  return ((m / 2) % 2 == 0) ? m + 2 : m;
-}
-
-template <int NX>
-struct PcgLayout {
-  static constexpr int BS = NX * NX, TRI = NX * (NX + 1) / 2;
-  static constexpr int BSP = pad_stride(BS), TRP = pad_stride(TRI);
-  static constexpr int VSTRIDE = NX;   // exchange vectors: NX doubles per block row (NX even)
-  __host__ __device__ static size_t vec_bytes(int nb) { return 2 * (size_t)(nb * NX + 2) * 8 + 64 * 16; }
-  __host__ __device__ static size_t mat_bytes(int N) {
-    return ((size_t)N * BSP + 2 * (size_t)(N + 1) * TRP) * 8;
-  }
-};
-
 // y += M v for a symmetric block in packed lower-triangular storage (row-major, 16-byte aligned)
 template <int NX>
 __device__ __forceinline__ void sym_apply_packed(const double* __restrict__ Mp, const double* v, double* y) {
@@ -623,23 +710,6 @@ __device__ __forceinline__ void sym_apply_packed(const double* __restrict__ Mp, 
       } else {
         m = cur.y;
       }
-      if (j < i) {
-        y[i] = fma(m, v[j], y[i]);
-        y[j] = fma(m, v[i], y[j]);
-      } else {
-        y[i] = fma(m, v[i], y[i]);
-      }
-    }
-  }
-}
-// same for a full row-major block of which only the lower triangle is read
-template <int NX>
-__device__ __forceinline__ void sym_apply_full(const double* __restrict__ Mf, const double* v, double* y) {
-#pragma unroll
-  for (int i = 0; i < NX; ++i) {
-#pragma unroll
-    for (int j = 0; j <= i; ++j) {
-      const double m = Mf[i * NX + j];
       if (j < i) {
         y[i] = fma(m, v[j], y[i]);
         y[j] = fma(m, v[i], y[j]);
@@ -700,7 +770,7 @@ template <int NX, int NU, bool SMEM_MATS>
 __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   static_assert(NX % 2 == 0, "state = [positions, velocities]");
   using L = PcgLayout<NX>;
-  constexpr int BS = L::BS, TRI = L::TRI;
+  constexpr int BS = L::BS;
   constexpr int HS = hinv_stride(NX, NU);
   const int b = blockIdx.x;
   int32_t* si = P.si + b * SI_WORDS;
@@ -721,69 +791,50 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   double* vB = vA + vlen + 2;            // exchange buffer: p
   double2* red = reinterpret_cast<double2*>(vB + vlen + 2);
   double* mats = reinterpret_cast<double*>(red + 64);
-  // block strides of the three matrix families as this kernel reads them
-  constexpr int OST = SMEM_MATS ? L::BSP : BS;
-  constexpr int SST = SMEM_MATS ? L::TRP : BS;     // S_kk: packed in smem, full (lower read) in global
-  constexpr int DST = SMEM_MATS ? L::TRP : TRI;    // D_k^-1: packed
-  const double *So, *Sd, *Di;
+  // per-solve matrix record written by k_schur: [phi | packed S_kk | packed D_k^-1]
+  constexpr int OST = L::BSP, SST = L::TRP, DST = L::TRP;
+  const double* pm = P.pmats + (size_t)b * L::mat_doubles(N);
+  __shared__ __align__(8) unsigned long long fill_bar;
   if constexpr (SMEM_MATS) {
-    double* sSo = mats;
-    double* sSd = sSo + (size_t)N * L::BSP;
-    double* sDi = sSd + (size_t)nb * L::TRP;
-    const double* gSo = P.Soff + (size_t)b * N * BS;
-    for (int idx = t; idx < N * (BS / 2); idx += blockDim.x) {
-      const int blk = idx / (BS / 2), w = idx % (BS / 2);
-      reinterpret_cast<double2*>(sSo + (size_t)blk * L::BSP)[w] = reinterpret_cast<const double2*>(gSo + (size_t)blk * BS)[w];
+    // one elected thread pulls the whole record into shared memory with bulk async copies
+    // (TMA, completion counted in bytes on an mbarrier); everyone else sets up meanwhile
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&fill_bar);
+    if (t == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const double* gSd = P.Sdiag + (size_t)b * nb * BS;
-    const double* gDi = P.Dinv + (size_t)b * nb * TRI;
-    for (int idx = t; idx < nb * TRI; idx += blockDim.x) {
-      const int blk = idx / TRI, w = idx % TRI;
-      // w -> (i, j) of the lower triangle
-      int i = 0;
-      while ((i + 1) * (i + 2) / 2 <= w) ++i;
-      const int j = w - i * (i + 1) / 2;
-      const double* Sf = gSd + (size_t)blk * BS;
-      sSd[(size_t)blk * L::TRP + w] = 0.5 * (Sf[i * NX + j] + Sf[j * NX + i]);
-      sDi[(size_t)blk * L::TRP + w] = gDi[(size_t)blk * TRI + w];
+    __syncthreads();
+    if (t == 0) {
+      const unsigned bytes_off = (unsigned)((size_t)N * L::BSP * 8);
+      const unsigned bytes_sym = (unsigned)((size_t)nb * L::TRP * 8);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes_off + 2 * bytes_sym)
+                   : "memory");
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(mats);
+      const char* src = reinterpret_cast<const char*>(pm);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "l"(src), "r"(bytes_off), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + bytes_off),
+          "l"(src + bytes_off), "r"(bytes_sym), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              dst + bytes_off + bytes_sym),
+          "l"(src + bytes_off + bytes_sym), "r"(bytes_sym), "r"(bar)
+          : "memory");
     }
-    So = sSo;
-    Sd = sSd;
-    Di = sDi;
-  } else {
-    So = P.Soff + (size_t)b * N * BS;
-    Sd = P.Sdiag + (size_t)b * nb * BS;
-    Di = P.Dinv + (size_t)b * nb * TRI;
   }
+  const double* So = SMEM_MATS ? mats : pm;
+  const double* Sd = So + (size_t)N * L::BSP;
+  const double* Di = Sd + (size_t)nb * L::TRP;
   const bool valid = t < nb;
   const int k = valid ? t : 0;
   BlockReducer R{red, 0, (int)((blockDim.x + 31) >> 5)};
 
-  auto apply_S_diag = [&](const double* v, double* y) {
-    if constexpr (SMEM_MATS) sym_apply_packed<NX>(Sd + (size_t)k * SST, v, y);
-    else sym_apply_full<NX>(Sd + (size_t)k * SST, v, y);
-  };
-  auto apply_D_inv = [&](const double* v, double* y) {
-    if constexpr (SMEM_MATS) sym_apply_packed<NX>(Di + (size_t)k * DST, v, y);
-    else {
-      // packed in global memory: 8-byte loads (blocks of TRI doubles are not 16-byte aligned)
-      const double* Mp = Di + (size_t)k * DST;
-      int idx = 0;
-#pragma unroll
-      for (int i = 0; i < NX; ++i) {
-#pragma unroll
-        for (int j = 0; j <= i; ++j, ++idx) {
-          const double m = Mp[idx];
-          if (j < i) {
-            y[i] = fma(m, v[j], y[i]);
-            y[j] = fma(m, v[i], y[j]);
-          } else {
-            y[i] = fma(m, v[i], y[i]);
-          }
-        }
-      }
-    }
-  };
+  auto apply_S_diag = [&](const double* v, double* y) { sym_apply_packed<NX>(Sd + (size_t)k * SST, v, y); };
+  auto apply_D_inv = [&](const double* v, double* y) { sym_apply_packed<NX>(Di + (size_t)k * DST, v, y); };
   // y += phi_{k-1} v_{k-1} + phi_k^T v_{k+1}, neighbours' vectors read from the exchange buffer
   auto apply_off = [&](const double* buf, double* y) {
     double vn[NX];
@@ -854,7 +905,18 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
 
   int its = 0, breakdown = 0;
   bool nan_curv = false;
-  double2 s = R.sum2(dot(r, r), viol_part);   // (also orders the shared-memory fill before first use)
+  if constexpr (SMEM_MATS) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&fill_bar);
+    unsigned done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+    }
+  }
+  double2 s = R.sum2(dot(r, r), viol_part);
   double res = sqrt(s.x);
   const double viol = s.y;
   if (!(res <= P.pcg_tol)) {
@@ -992,7 +1054,9 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
       info[GATO_INFO_N_RECORDS] = it + 1;
       info[GATO_INFO_CONVERGED] = 1;
       si[SI_ACTIVE] = 0;
-      si[SI_SKIP_LS] = 1;
+      // first iteration of the solve: merit(X0, U0) is produced by this pass's alpha = 0
+      // candidate; k_update patches it into the record (SKIP_LS = 2)
+      si[SI_SKIP_LS] = si[SI_MERIT_VALID] ? 1 : 2;
     } else {
       si[SI_SKIP_LS] = 0;
     }
@@ -1003,21 +1067,26 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
 // k_linesearch: merit of every candidate (sqp.py:132-166).  grid (C, M), one thread per stage
 // knot: candidate point (X + a dX, U + a dU), one RK4 prediction, |defect|_1, quadratic cost
 // with the undamped weights; fixed-tree reduction over knots.  Non-finite candidates -> +inf.
-// `init` = 1 evaluates only candidate 0 at alpha = 0 (the initial merit, sqp.py:229).
+// grid (C + 1, M): the extra candidate is alpha = 0, evaluated only while merit(X0, U0) is unknown.
 // -----------------------------------------------------------------------------------------
 template <class Mdl>
-__global__ void __launch_bounds__(128) k_linesearch(SolveParams P, int init) {
+__global__ void __launch_bounds__(128) k_linesearch(SolveParams P) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU, NF = Mdl::NF;
   const int c = blockIdx.x, b = blockIdx.y;
   const int32_t* si = P.si + b * SI_WORDS;
-  if (!si[SI_ACTIVE]) return;
-  if (!init && si[SI_SKIP_LS]) return;
+  const int skip = si[SI_SKIP_LS];
+  if (c < P.C) {
+    if (!si[SI_ACTIVE] || skip) return;
+  } else {
+    // candidate C is the current iterate (alpha = 0): merit(X0, U0) of sqp.py:229, needed once
+    if (!((si[SI_ACTIVE] && !skip && !si[SI_MERIT_VALID]) || skip == 2)) return;
+  }
   __shared__ double2 red[2 * 32];
   __shared__ int bad_flag;
   if (threadIdx.x == 0) bad_flag = 0;
   __syncthreads();
   const int N = P.N, nb = N + 1;
-  const double alpha = init ? 0.0 : P.alphas[c];
+  const double alpha = (c < P.C) ? P.alphas[c] : 0.0;
   double cost = 0.0, viol = 0.0;
   int bad = 0;
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
@@ -1089,8 +1158,8 @@ __global__ void __launch_bounds__(128) k_linesearch(SolveParams P, int init) {
   if (threadIdx.x == 0) {
     double value = s.x + P.mu * s.y;
     if (bad_flag || !isfinite(value)) value = INFINITY;
-    P.merits[(size_t)b * P.C + c] = value;
-    P.viols[(size_t)b * P.C + c] = s.y;
+    P.merits[(size_t)b * (P.C + 1) + c] = value;
+    P.viols[(size_t)b * (P.C + 1) + c] = s.y;
   }
 }
 
