@@ -68,11 +68,17 @@ __global__ void __launch_bounds__(128) k_update(SolveParams P, int nx, int nu, c
       }
       int best = 0;
       double bm = mer[0];
-      for (int c = 1; c < P.C; ++c)
-        if (mer[c] < bm) {
-          bm = mer[c];
-          best = c;
-        }
+      for (int c0 = 1; c0 < P.C; c0 += 8) {   // loads of a chunk issue together; first minimum wins
+        double m[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m[i] = (c0 + i < P.C) ? mer[c0 + i] : INFINITY;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (c0 + i < P.C && m[i] < bm) {
+            bm = m[i];
+            best = c0 + i;
+          }
+      }
       // np.argmin returns the first NaN if any; merits are never NaN (non-finite -> +inf)
       const double cur = P.sd[b * SD_WORDS + SD_MERIT];
       const int accepted = bm < cur;

@@ -425,7 +425,7 @@ struct SchurSmem {
 };
 
 template <int NX, int NU, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 4) k_schur(SolveParams P) {
+__global__ void __launch_bounds__(WARPS * 32, 3) k_schur(SolveParams P) {
   extern __shared__ __align__(16) double schur_smem_raw[];
   using L = PcgLayout<NX>;
   constexpr int HALF = NX / 2;
@@ -505,18 +505,48 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_schur(SolveParams P) {
     const int j = k - 1;
     const double* Ag = P.A + ((size_t)b * P.N + j) * NX * NX;
     const double* Bg = P.B + ((size_t)b * P.N + j) * NX * NU;
-    for (int idx = lane; idx < NX * NX; idx += 32) {
-      const double v = Ag[idx];
-      S.A[idx] = v;
-      S.AT[(idx % NX) * NX + idx / NX] = v;
-      S.Q[idx] = Qi[idx];
+    {   // stage A, A^T, Q^-1, B, B^T, R^-1: all global loads issued before the first use
+      constexpr int RA = (NX * NX + 31) / 32, RB = (NX * NU + 31) / 32, RR = (NU * NU + 31) / 32;
+      double va[RA], vq[RA], vb[RB], vr[RR];
+#pragma unroll
+      for (int i = 0; i < RA; ++i) {
+        const int idx = lane + 32 * i;
+        va[i] = (idx < NX * NX) ? Ag[idx] : 0.0;
+        vq[i] = (idx < NX * NX) ? Qi[idx] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const int idx = lane + 32 * i;
+        vb[i] = (idx < NX * NU) ? Bg[idx] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < RR; ++i) {
+        const int idx = lane + 32 * i;
+        vr[i] = (idx < NU * NU) ? Ri[idx] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < RA; ++i) {
+        const int idx = lane + 32 * i;
+        if (idx < NX * NX) {
+          S.A[idx] = va[i];
+          S.AT[(idx % NX) * NX + idx / NX] = va[i];
+          S.Q[idx] = vq[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const int idx = lane + 32 * i;
+        if (idx < NX * NU) {
+          S.B[idx] = vb[i];
+          S.BT[(idx % NU) * NX + idx / NU] = vb[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RR; ++i) {
+        const int idx = lane + 32 * i;
+        if (idx < NU * NU) S.R[idx] = vr[i];
+      }
     }
-    for (int idx = lane; idx < NX * NU; idx += 32) {
-      const double v = Bg[idx];
-      S.B[idx] = v;
-      S.BT[(idx % NU) * NX + idx / NU] = v;
-    }
-    for (int idx = lane; idx < NU * NU; idx += 32) S.R[idx] = Ri[idx];
     __syncwarp();
     const int r = lane >> 1, c0 = (lane & 1) * HALF;
     const bool strip = lane < 2 * NX;
@@ -693,66 +723,140 @@ struct BlockReducer {
   }
 };
 
-// y += M v for a symmetric block in packed lower-triangular storage (row-major, 16-byte aligned)
-template <int NX>
-__device__ __forceinline__ void sym_apply_packed(const double* __restrict__ Mp, const double* v, double* y) {
-  const double2* M2 = reinterpret_cast<const double2*>(Mp);
-  double2 cur = make_double2(0.0, 0.0);
-  int idx = 0;
+// ---- block-row slices -------------------------------------------------------------------
+// A block row is owned by T threads (T = 1 or 2); thread slice TS owns rows [TS*RP, (TS+1)*RP),
+// RP = NX / T, of every vector and of every product.  TS is uniform within a warp (warps
+// alternate slices), so the slice-specialised code below never diverges.
+
+// element `idx` of a 16-byte aligned packed array, pairing even/odd neighbours into one 128-bit load
+struct PackedStream {
+  const double2* base;
+  double2 cur;
+  __device__ __forceinline__ explicit PackedStream(const double* p) : base(reinterpret_cast<const double2*>(p)) {
+    cur = make_double2(0.0, 0.0);
+  }
+  // must be called with consecutive idx values inside one fully unrolled loop nest
+  __device__ __forceinline__ double next(int idx, bool first) {
+    if ((idx & 1) == 0 || first) cur = base[idx >> 1];
+    return (idx & 1) ? cur.y : cur.x;
+  }
+};
+
+// y[RP] += (M v)[slice] for a symmetric block M in packed lower-triangular storage; v is the
+// full NX-vector of the block row.
+template <int NX, int T, int TS>
+__device__ __forceinline__ void sym_apply_slice(const double* __restrict__ Mp, const double* v, double* y) {
+  constexpr int RP = NX / T, R0 = TS * RP;
+  if constexpr (T == 1) {
+    PackedStream st(Mp);
+    int idx = 0;
 #pragma unroll
-  for (int i = 0; i < NX; ++i) {
+    for (int i = 0; i < NX; ++i) {
 #pragma unroll
-    for (int j = 0; j <= i; ++j, ++idx) {
-      double m;
-      if ((idx & 1) == 0) {
-        cur = M2[idx >> 1];
-        m = cur.x;
-      } else {
-        m = cur.y;
+      for (int j = 0; j <= i; ++j, ++idx) {
+        const double m = st.next(idx, idx == 0);
+        if (j < i) {
+          y[i] = fma(m, v[j], y[i]);
+          y[j] = fma(m, v[i], y[j]);
+        } else {
+          y[i] = fma(m, v[i], y[i]);
+        }
       }
-      if (j < i) {
-        y[i] = fma(m, v[j], y[i]);
-        y[j] = fma(m, v[i], y[j]);
-      } else {
-        y[i] = fma(m, v[i], y[i]);
+    }
+  } else if constexpr (TS == 0) {
+    // rows [0, RP): own symmetric sub-block, then the transposed use of rows [RP, NX) x cols [0, RP)
+    PackedStream st(Mp);
+    int idx = 0;
+#pragma unroll
+    for (int i = 0; i < RP; ++i) {
+#pragma unroll
+      for (int j = 0; j <= i; ++j, ++idx) {
+        const double m = st.next(idx, idx == 0);
+        if (j < i) {
+          y[i] = fma(m, v[j], y[i]);
+          y[j] = fma(m, v[i], y[j]);
+        } else {
+          y[i] = fma(m, v[i], y[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = RP; i < NX; ++i) {
+      const int row = i * (i + 1) / 2;
+#pragma unroll
+      for (int j = 0; j < RP; ++j) y[j] = fma(Mp[row + j], v[i], y[j]);
+    }
+  } else {
+    // rows [RP, NX): a contiguous stream of the packed storage
+    PackedStream st(Mp);
+#pragma unroll
+    for (int i = R0; i < NX; ++i) {
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        const int idx = i * (i + 1) / 2 + j;
+        const double m = st.next(idx, i == R0 && j == 0);
+        if (j < R0) {
+          y[i - R0] = fma(m, v[j], y[i - R0]);
+        } else if (j < i) {
+          y[i - R0] = fma(m, v[j], y[i - R0]);
+          y[j - R0] = fma(m, v[i], y[j - R0]);
+        } else {
+          y[i - R0] = fma(m, v[i], y[i - R0]);
+        }
       }
     }
   }
 }
-// y += O v (row i of O against v) and y += O^T v (row j of O scaled by v[j]); O row-major
-template <int NX>
-__device__ __forceinline__ void off_apply_rows(const double* __restrict__ O, const double* v, double* y) {
+// y[RP] += (O v)[slice]: rows R0.. of the row-major block O against the full vector v
+template <int NX, int T, int TS>
+__device__ __forceinline__ void off_rows_slice(const double* __restrict__ O, const double* v, double* y) {
+  constexpr int RP = NX / T, R0 = TS * RP;
 #pragma unroll
-  for (int i = 0; i < NX; ++i) {
-    const double2* r2 = reinterpret_cast<const double2*>(O + i * NX);
-    double acc = 0.0;
+  for (int i = 0; i < RP; ++i) {
+    const double2* r2 = reinterpret_cast<const double2*>(O + (R0 + i) * NX);
+    double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
     for (int j = 0; j < NX / 2; ++j) {
       const double2 a = r2[j];
-      acc = fma(a.x, v[2 * j], acc);
-      acc = fma(a.y, v[2 * j + 1], acc);
+      acc0 = fma(a.x, v[2 * j], acc0);
+      acc1 = fma(a.y, v[2 * j + 1], acc1);
     }
-    y[i] += acc;
+    y[i] += acc0 + acc1;
   }
 }
-template <int NX>
-__device__ __forceinline__ void off_apply_cols(const double* __restrict__ O, const double* v, double* y) {
+// y[RP] += (O^T v)[slice]: for every row j of O, the segment of columns R0.. scaled by v[j]
+template <int NX, int T, int TS>
+__device__ __forceinline__ void off_cols_slice(const double* __restrict__ O, const double* v, double* y) {
+  constexpr int RP = NX / T, R0 = TS * RP;
 #pragma unroll
   for (int j = 0; j < NX; ++j) {
-    const double2* r2 = reinterpret_cast<const double2*>(O + j * NX);
     const double vj = v[j];
-#pragma unroll
-    for (int i = 0; i < NX / 2; ++i) {
-      const double2 a = r2[i];
-      y[2 * i] = fma(a.x, vj, y[2 * i]);
-      y[2 * i + 1] = fma(a.y, vj, y[2 * i + 1]);
+    const double* seg = O + j * NX + R0;   // NX even: seg is 16-byte aligned iff R0 is even
+    int i = 0;
+    if constexpr (R0 % 2 == 1) {
+      y[0] = fma(seg[0], vj, y[0]);
+      i = 1;
     }
+#pragma unroll
+    for (; i + 1 < RP; i += 2) {
+      const double2 a = *reinterpret_cast<const double2*>(seg + i);
+      y[i] = fma(a.x, vj, y[i]);
+      y[i + 1] = fma(a.y, vj, y[i + 1]);
+    }
+    if (i < RP) y[i] = fma(seg[i], vj, y[i]);
   }
 }
-template <int NX>
-__device__ __forceinline__ void vec_store(double* dst, const double* v) {
+// slice of an exchange vector: store own RP entries, load a full NX-vector
+template <int NX, int T, int TS>
+__device__ __forceinline__ void slice_store(double* blk, const double* v) {
+  constexpr int RP = NX / T, R0 = TS * RP;
+  if constexpr (R0 % 2 == 0 && RP % 2 == 0) {
 #pragma unroll
-  for (int j = 0; j < NX / 2; ++j) reinterpret_cast<double2*>(dst)[j] = make_double2(v[2 * j], v[2 * j + 1]);
+    for (int j = 0; j < RP / 2; ++j) reinterpret_cast<double2*>(blk + R0)[j] = make_double2(v[2 * j], v[2 * j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < RP; ++j) blk[R0 + j] = v[j];
+  }
 }
 template <int NX>
 __device__ __forceinline__ void vec_load(const double* src, double* v) {
@@ -766,11 +870,14 @@ __device__ __forceinline__ void vec_load(const double* src, double* v) {
 
 constexpr int kPcgMaxThreads = 256;
 
-template <int NX, int NU, bool SMEM_MATS>
+// host+device: threads of the PCG CTA for horizon N with T threads per block row
+__host__ __device__ constexpr int pcg_threads(int N, int T) { return T * (((N + 1) + 31) / 32) * 32; }
+
+template <int NX, int NU, bool SMEM_MATS, int T>
 __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
-  static_assert(NX % 2 == 0, "state = [positions, velocities]");
+  static_assert(NX % 2 == 0 && NX % T == 0, "state = [positions, velocities]; T divides NX");
   using L = PcgLayout<NX>;
-  constexpr int BS = L::BS;
+  constexpr int BS = L::BS, RP = NX / T;
   constexpr int HS = hinv_stride(NX, NU);
   const int b = blockIdx.x;
   int32_t* si = P.si + b * SI_WORDS;
@@ -787,7 +894,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   }
   extern __shared__ __align__(16) double pcg_smem[];
   const int vlen = nb * NX;
-  double* vA = pcg_smem;                 // exchange buffer: w, later lambda
+  double* vA = pcg_smem;                 // exchange buffer: w, later lambda / grad_x
   double* vB = vA + vlen + 2;            // exchange buffer: p
   double2* red = reinterpret_cast<double2*>(vB + vlen + 2);
   double* mats = reinterpret_cast<double*>(red + 64);
@@ -829,82 +936,123 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   const double* So = SMEM_MATS ? mats : pm;
   const double* Sd = So + (size_t)N * L::BSP;
   const double* Di = Sd + (size_t)nb * L::TRP;
-  const bool valid = t < nb;
-  const int k = valid ? t : 0;
+
+  // thread -> (block row k, slice ts): warps alternate slices, lanes run over block rows
+  const int warp = t >> 5, lane = t & 31;
+  const int ts = warp % T;
+  const int krow = (warp / T) * 32 + lane;
+  const bool valid = krow < nb;
+  const int k = valid ? krow : 0;
+  const int r0 = ts * RP;
   BlockReducer R{red, 0, (int)((blockDim.x + 31) >> 5)};
 
-  auto apply_S_diag = [&](const double* v, double* y) { sym_apply_packed<NX>(Sd + (size_t)k * SST, v, y); };
-  auto apply_D_inv = [&](const double* v, double* y) { sym_apply_packed<NX>(Di + (size_t)k * DST, v, y); };
+  // slice-dispatched block operations (ts is warp-uniform)
+  auto sym_apply = [&](const double* Mp, const double* v, double* y) {
+    if constexpr (T == 1) sym_apply_slice<NX, 1, 0>(Mp, v, y);
+    else if (ts == 0) sym_apply_slice<NX, T, 0>(Mp, v, y);
+    else sym_apply_slice<NX, T, 1>(Mp, v, y);
+  };
+  auto off_rows = [&](const double* O, const double* v, double* y) {
+    if constexpr (T == 1) off_rows_slice<NX, 1, 0>(O, v, y);
+    else if (ts == 0) off_rows_slice<NX, T, 0>(O, v, y);
+    else off_rows_slice<NX, T, 1>(O, v, y);
+  };
+  auto off_cols = [&](const double* O, const double* v, double* y) {
+    if constexpr (T == 1) off_cols_slice<NX, 1, 0>(O, v, y);
+    else if (ts == 0) off_cols_slice<NX, T, 0>(O, v, y);
+    else off_cols_slice<NX, T, 1>(O, v, y);
+  };
+  auto store_slice = [&](double* buf, const double* v) {
+    if constexpr (T == 1) slice_store<NX, 1, 0>(buf + k * NX, v);
+    else if (ts == 0) slice_store<NX, T, 0>(buf + k * NX, v);
+    else slice_store<NX, T, 1>(buf + k * NX, v);
+  };
   // y += phi_{k-1} v_{k-1} + phi_k^T v_{k+1}, neighbours' vectors read from the exchange buffer
   auto apply_off = [&](const double* buf, double* y) {
     double vn[NX];
     if (k > 0) {
       vec_load<NX>(buf + (k - 1) * NX, vn);
-      off_apply_rows<NX>(So + (size_t)(k - 1) * OST, vn, y);
+      off_rows(So + (size_t)(k - 1) * OST, vn, y);
     }
     if (k < N) {
       vec_load<NX>(buf + (k + 1) * NX, vn);
-      off_apply_cols<NX>(So + (size_t)k * OST, vn, y);
+      off_cols(So + (size_t)k * OST, vn, y);
     }
   };
 
-  double lam[NX], r[NX], p[NX], z[NX];
+  double lam[RP], r[RP], p[RP], z[RP];
   {
-    const double* gam = P.gamma + (size_t)b * vlen + k * NX;
+    const double* gam = P.gamma + (size_t)b * vlen + k * NX + r0;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) {
+    for (int i = 0; i < RP; ++i) {
       lam[i] = 0.0;
       r[i] = valid ? gam[i] : 0.0;
       p[i] = 0.0;
+      z[i] = 0.0;
     }
   }
   // violation of the current iterate: |x_s - x_0|_1 + sum |e|_1  (sqp.py:111-115)
   double viol_part = 0.0;
   if (valid) {
     if (k < N) {
-      const double* eb = P.e + ((size_t)b * N + k) * NX;
+      const double* eb = P.e + ((size_t)b * N + k) * NX + r0;
 #pragma unroll
-      for (int i = 0; i < NX; ++i) viol_part += fabs(eb[i]);
+      for (int i = 0; i < RP; ++i) viol_part += fabs(eb[i]);
     }
     if (k == 0) {
-      const double* xs = P.x_start + (size_t)b * NX;
-      const double* x0 = P.X + (size_t)b * nb * NX;
+      const double* xs = P.x_start + (size_t)b * NX + r0;
+      const double* x0 = P.X + (size_t)b * nb * NX + r0;
 #pragma unroll
-      for (int i = 0; i < NX; ++i) viol_part += fabs(xs[i] - x0[i]);
+      for (int i = 0; i < RP; ++i) viol_part += fabs(xs[i] - x0[i]);
     }
   }
   auto dot = [&](const double* a, const double* c) {
     double acc = 0.0;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) acc = fma(a[i], c[i], acc);
+    for (int i = 0; i < RP; ++i) acc = fma(a[i], c[i], acc);
     return acc;
   };
-  // z = Phi^-1 r (thread-private result); one barrier
+  // z = Phi^-1 r (thread-private slice).  T = 1: one barrier; T = 2: r, w and u are exchanged.
   auto precondition = [&]() {
-    double w[NX];
+    double full[NX], w[RP], u[RP];
 #pragma unroll
-    for (int i = 0; i < NX; ++i) w[i] = 0.0;
-    if (valid) {
-      apply_D_inv(r, w);
-      vec_store<NX>(vA + k * NX, w);
-    }
-    __syncthreads();
-    double u[NX];
+    for (int i = 0; i < RP; ++i) w[i] = u[i] = z[i] = 0.0;
+    if constexpr (T == 1) {
+      if (valid) {
+        sym_apply(Di + (size_t)k * DST, r, w);
+        store_slice(vA, w);
+      }
+      __syncthreads();
+      if (valid) {
+        apply_off(vA, u);
 #pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      u[i] = 0.0;
-      z[i] = 0.0;
-    }
-    if (valid) {
-      apply_off(vA, u);
+        for (int i = 0; i < RP; ++i) u[i] = r[i] - u[i];
+        sym_apply(Di + (size_t)k * DST, u, z);
+      }
+    } else {
+      // r -> vA, w -> vB (free between two S p products), u -> vA: three barriers
+      if (valid) store_slice(vA, r);
+      __syncthreads();
+      if (valid) {
+        vec_load<NX>(vA + k * NX, full);
+        sym_apply(Di + (size_t)k * DST, full, w);
+        store_slice(vB, w);
+      }
+      __syncthreads();   // also: every read of r in vA is done
+      if (valid) {
+        apply_off(vB, u);
 #pragma unroll
-      for (int i = 0; i < NX; ++i) u[i] = r[i] - u[i];
-      apply_D_inv(u, z);
+        for (int i = 0; i < RP; ++i) u[i] = r[i] - u[i];
+        store_slice(vA, u);
+      }
+      __syncthreads();
+      if (valid) {
+        vec_load<NX>(vA + k * NX, full);
+        sym_apply(Di + (size_t)k * DST, full, z);
+      }
     }
   };
 
-  int its = 0, breakdown = 0;
-  bool nan_curv = false;
   if constexpr (SMEM_MATS) {
     const unsigned bar = (unsigned)__cvta_generic_to_shared(&fill_bar);
     unsigned done = 0;
@@ -916,23 +1064,31 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
           : "memory");
     }
   }
+  int its = 0, breakdown = 0;
+  bool nan_curv = false;
   double2 s = R.sum2(dot(r, r), viol_part);
   double res = sqrt(s.x);
   const double viol = s.y;
   if (!(res <= P.pcg_tol)) {
     precondition();
 #pragma unroll
-    for (int i = 0; i < NX; ++i) p[i] = z[i];
+    for (int i = 0; i < RP; ++i) p[i] = z[i];
     double rz = R.sum2(dot(r, z), 0.0).x;
     const int cap = P.pcg_cap;
     for (int it = 1; it <= cap; ++it) {
-      if (valid) vec_store<NX>(vB + k * NX, p);
+      if (valid) store_slice(vB, p);
       __syncthreads();
-      double q[NX];
+      double q[RP];
 #pragma unroll
-      for (int i = 0; i < NX; ++i) q[i] = 0.0;
+      for (int i = 0; i < RP; ++i) q[i] = 0.0;
       if (valid) {
-        apply_S_diag(p, q);
+        if constexpr (T == 1) {
+          sym_apply(Sd + (size_t)k * SST, p, q);
+        } else {
+          double full[NX];
+          vec_load<NX>(vB + k * NX, full);
+          sym_apply(Sd + (size_t)k * SST, full, q);
+        }
         apply_off(vB, q);
       }
       const double curv = R.sum2(dot(p, q), 0.0).x;
@@ -947,7 +1103,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
       }
       const double a = rz / curv;
 #pragma unroll
-      for (int i = 0; i < NX; ++i) {
+      for (int i = 0; i < RP; ++i) {
         lam[i] = lam[i] + a * p[i];
         r[i] = r[i] - a * q[i];
       }
@@ -958,13 +1114,13 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
       if (res <= P.pcg_tol) break;
       const double beta = rr.x / rz;
 #pragma unroll
-      for (int i = 0; i < NX; ++i) p[i] = z[i] + beta * p[i];
+      for (int i = 0; i < RP; ++i) p[i] = z[i] + beta * p[i];
       rz = rr.x;
     }
   }
   if (nan_curv) {
 #pragma unroll
-    for (int i = 0; i < NX; ++i) lam[i] = nan("");
+    for (int i = 0; i < RP; ++i) lam[i] = nan("");
   }
 
   if (breakdown) {
@@ -984,49 +1140,54 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   // ---- recover_step (qpform.py:375-397).  -Q^-1 A_k^T lam_{k+1} = phi_k^T lam_{k+1} reuses the
   // resident sub-diagonal blocks instead of re-reading A_k from global memory. ----
   __syncthreads();
+  const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
   if (valid) {
-    vec_store<NX>(vA + k * NX, lam);
-    double* lg = P.lam + (size_t)b * vlen + k * NX;
+    store_slice(vA, lam);
+    double gxs[RP];
 #pragma unroll
-    for (int i = 0; i < NX; ++i) lg[i] = lam[i];
+    for (int i = 0; i < RP; ++i) gxs[i] = g[r0 + i] - lam[i];
+    store_slice(vB, gxs);
+    double* lg = P.lam + (size_t)b * vlen + k * NX + r0;
+#pragma unroll
+    for (int i = 0; i < RP; ++i) lg[i] = lam[i];
   }
   __syncthreads();
   const double* hinv = P.hinv + (size_t)b * HS;
   double step_part = 0.0;
   if (valid) {
-    const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
-    double gx[NX], dx[NX], ln[NX];
-#pragma unroll
-    for (int i = 0; i < NX; ++i) gx[i] = g[i] - lam[i];
+    double gx[NX], dx[RP], ln[NX];
+    vec_load<NX>(vB + k * NX, gx);
     const double* Qk = (k < N) ? hinv : hinv + BS;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) dx[i] = -dot_row<NX>(Qk + i * NX, gx);
+    for (int i = 0; i < RP; ++i) dx[i] = -dot_row<NX>(Qk + (r0 + i) * NX, gx);
     if (k < N) {
       vec_load<NX>(vA + (k + 1) * NX, ln);
-      off_apply_cols<NX>(So + (size_t)k * OST, ln, dx);
-      const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
-      const double* Ri = hinv + 2 * BS;
-      double gu[NU];
+      off_cols(So + (size_t)k * OST, ln, dx);
+      if (ts == 0) {   // the control step of this knot (slice 0 only)
+        const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
+        const double* Ri = hinv + 2 * BS;
+        double gu[NU];
 #pragma unroll
-      for (int ju = 0; ju < NU; ++ju) gu[ju] = g[NX + ju];
+        for (int ju = 0; ju < NU; ++ju) gu[ju] = g[NX + ju];
 #pragma unroll
-      for (int j = 0; j < NX; ++j) {
+        for (int j = 0; j < NX; ++j) {
 #pragma unroll
-        for (int ju = 0; ju < NU; ++ju) gu[ju] = fma(Bk[j * NU + ju], ln[j], gu[ju]);
-      }
-      double* dU = P.dU + ((size_t)b * N + k) * NU;
+          for (int ju = 0; ju < NU; ++ju) gu[ju] = fma(Bk[j * NU + ju], ln[j], gu[ju]);
+        }
+        double* dU = P.dU + ((size_t)b * N + k) * NU;
 #pragma unroll
-      for (int ju = 0; ju < NU; ++ju) {
-        double acc = 0.0;
+        for (int ju = 0; ju < NU; ++ju) {
+          double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
-        dU[ju] = -acc;
-        step_part = nanmax(step_part, fabs(acc));
+          for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
+          dU[ju] = -acc;
+          step_part = nanmax(step_part, fabs(acc));
+        }
       }
     }
-    double* dX = P.dX + ((size_t)b * nb + k) * NX;
+    double* dX = P.dX + ((size_t)b * nb + k) * NX + r0;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) {
+    for (int i = 0; i < RP; ++i) {
       dX[i] = dx[i];
       step_part = nanmax(step_part, fabs(dx[i]));
     }
