@@ -57,6 +57,18 @@ def flops_solve_iteration(N, P, C=9):
     return N * F_LIN + N * F_SCHUR + (N + 1) * F_PREC + P * f_pcg(N) + N * F_REC + C * N * F_LS + F_HESS
 
 
+def ncu_traffic(workload, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the newest committed
+    `ncu --set full` capture of this workload (profiles/rNN_ncu_kernels.json); None if not captured."""
+    files = sorted((ROOT / "profiles").glob("r*_ncu_kernels.json"))
+    for f in reversed(files):
+        try:
+            return float(json.loads(f.read_text())[workload][kernel]["dram_bytes_per_launch"])
+        except Exception:
+            continue
+    return None
+
+
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -419,7 +431,8 @@ def run_gpu_arm(args, w, rank, local_rank, world):
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                 "peak_source": "in-run DFMA probe (gato_measure_fp64_peak); MEASURED_PEAKS.json carries no fp64 figure",
                 "launch_ms": fam_ms[dominant] / launches_dom, "algorithmic_flops_per_launch": fam_flops[dominant] / launches_dom,
-                "traffic": None,
+                "traffic": ncu_traffic(args.workload, {"linearize": "k_lin_tangent_iiwa", "schur": "k_schur",
+                                                       "pcg": "k_pcg", "linesearch": "k_linesearch"}[dominant]),
                 "hbm": {"achieved": alg_bytes / (kern_ms["total"] * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                         "frac": alg_bytes / (kern_ms["total"] * 1e-3) / 1e9 / hbm_peak, "peak_source": hbm_src,
                         "algorithmic_bytes_per_step": alg_bytes},
