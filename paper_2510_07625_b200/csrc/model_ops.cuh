@@ -85,9 +85,24 @@ int pcg_slices(int N) {
   return T;
 }
 
+// real-time variant (matrix rows in registers) whenever the horizon fits; GATO_PCG_RT=0 disables
+template <class Mdl>
+bool pcg_use_rt(int N) {
+  static int allowed = -1;
+  if (allowed < 0) allowed = env_int("GATO_PCG_RT", 1);
+  return allowed && Mdl::NX >= 14 && pcg_rt_threads(N, Mdl::NX) <= kPcgRtMaxThreads &&
+         pcg_rt_smem_bytes<Mdl::NX>(N) <= kMaxSmem;
+}
+
 template <class Mdl>
 cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU;
+  if constexpr (NX >= 14) {
+    if (pcg_use_rt<Mdl>(P.N)) {
+      k_pcg_rt<NX, NU><<<P.M, pcg_rt_threads(P.N, NX), pcg_rt_smem_bytes<NX>(P.N), s>>>(P);
+      return cudaGetLastError();
+    }
+  }
   int T = pcg_slices<Mdl>(P.N);
   if (pcg_threads(P.N, T) > kPcgMaxThreads) T = 1;
   const int threads = pcg_threads(P.N, T);
@@ -147,6 +162,13 @@ cudaError_t prepare_attrs(const SolveParams& P) {
   }
   const size_t bytes = pcg_smem_bytes<NX>(P.N, false);
   if (bytes > 48 * 1024) return cudaErrorInvalidConfiguration;
+  if constexpr (NX >= 14) {
+    if (pcg_rt_smem_bytes<NX>(P.N) <= kMaxSmem) {
+      err = cudaFuncSetAttribute(k_pcg_rt<NX, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pcg_rt_smem_bytes<NX>(P.N));
+      if (err != cudaSuccess) return err;
+    }
+  }
   return cudaSuccess;
 }
 

@@ -1225,6 +1225,294 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
 }
 
 // -----------------------------------------------------------------------------------------
+// k_pcg_rt: the PCG of the real-time regime (short horizons, few solves: latency bound).
+//
+// One CTA per solve, thread (k, i) owns rows i and i + NX/2 of block row k, and -- unlike k_pcg --
+// every matrix row the thread ever multiplies lives in its REGISTERS for the whole solve: its two
+// rows of S_kk, of phi_{k-1} and of phi_k^T (84 doubles at n = 14).  The PCG iteration then reads
+// shared memory only for vectors and for the two rows of D_k^-1, the serial work per thread per
+// iteration drops from ~1300 instructions (k_pcg, two threads per block row) to ~300, and 8 warps
+// per SM hide each other's latency.  Needs (N+1) * NX/2 <= 256 threads x 255 registers, i.e.
+// N <= 35 at n = 14; longer horizons use k_pcg.  Same factored preconditioner, same recurrence
+// stop test, same fixed-order reductions, same epilogue (step recovery, exit test) as k_pcg.
+// -----------------------------------------------------------------------------------------
+template <int NX>
+__device__ __forceinline__ double dot_reg(const double (&row)[NX], const double* __restrict__ v) {
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < NX / 2; ++j) {
+    const double2 c = v2[j];
+    a0 = fma(row[2 * j], c.x, a0);
+    a1 = fma(row[2 * j + 1], c.y, a1);
+  }
+  return a0 + a1;
+}
+
+constexpr int kPcgRtMaxThreads = 256;
+__host__ __device__ constexpr int pcg_rt_threads(int N, int NX) { return (((N + 1) * (NX / 2)) + 31) / 32 * 32; }
+template <int NX>
+__host__ __device__ constexpr size_t pcg_rt_smem_bytes(int N) {
+  return (3 * (size_t)((N + 1) * NX + 2) + (size_t)(N + 1) * NX * NX) * 8 + 64 * 16;
+}
+
+template <int NX, int NU>
+__global__ void __launch_bounds__(kPcgRtMaxThreads, 1) k_pcg_rt(SolveParams P) {
+  constexpr int HN = NX / 2, BS = NX * NX, TRI = NX * (NX + 1) / 2;
+  constexpr int HS = hinv_stride(NX, NU);
+  const int b = blockIdx.x;
+  int32_t* si = P.si + b * SI_WORDS;
+  if (!si[SI_ACTIVE]) return;
+  const int N = P.N, nb = N + 1;
+  const int t = threadIdx.x;
+  if (si[SI_SCHUR_FAIL] != INT_MAX) {
+    if (t == 0) {
+      const int key = si[SI_SCHUR_FAIL];
+      si[SI_SCHUR_FAIL] = INT_MAX;
+      record_failure(P, b, GATO_STATUS_FACTORIZATION, key / 64, GATO_BLOCK_S, key % 64, 0);
+    }
+    return;
+  }
+  extern __shared__ __align__(16) double pcg_smem[];
+  const int vlen = nb * NX;
+  double* vp = pcg_smem;            // p, later lambda
+  double* vr = vp + vlen + 2;       // r, then r - t, later grad_x
+  double* vw = vr + vlen + 2;       // w = D^-1 r, later grad_u
+  double2* red = reinterpret_cast<double2*>(vw + vlen + 2);
+  double* sD = reinterpret_cast<double*>(red + 64);   // D_k^-1, full row-major blocks
+
+  const bool valid = t < nb * HN;
+  const int k = valid ? t / HN : 0;
+  const int i0 = valid ? t % HN : 0, i1 = i0 + HN;
+  BlockReducer R{red, 0, (int)((blockDim.x + 31) >> 5)};
+
+  // ---- one-time fill: matrix rows -> registers, D^-1 -> shared memory ----
+  double sd0[NX], sd1[NX], ol0[NX], ol1[NX], ou0[NX], ou1[NX];
+  {
+    const double* Sdk = P.Sdiag + ((size_t)b * nb + k) * BS;
+    const double* Olo = P.Soff + ((size_t)b * N + (k > 0 ? k - 1 : 0)) * BS;
+    const double* Oup = P.Soff + ((size_t)b * N + (k < N ? k : 0)) * BS;
+    const bool has_lo = valid && k > 0, has_up = valid && k < N;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      sd0[j] = valid ? Sdk[i0 * NX + j] : 0.0;
+      sd1[j] = valid ? Sdk[i1 * NX + j] : 0.0;
+      ol0[j] = has_lo ? Olo[i0 * NX + j] : 0.0;
+      ol1[j] = has_lo ? Olo[i1 * NX + j] : 0.0;
+      ou0[j] = has_up ? Oup[j * NX + i0] : 0.0;   // row i of phi_k^T = column i of phi_k
+      ou1[j] = has_up ? Oup[j * NX + i1] : 0.0;
+    }
+    if (valid) {
+      const double* Dp = P.Dinv + ((size_t)b * nb + k) * TRI;
+      double* D = sD + (size_t)k * BS;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        D[i0 * NX + j] = Dp[(j <= i0) ? i0 * (i0 + 1) / 2 + j : j * (j + 1) / 2 + i0];
+        D[i1 * NX + j] = Dp[(j <= i1) ? i1 * (i1 + 1) / 2 + j : j * (j + 1) / 2 + i1];
+      }
+    }
+  }
+  const double* Dk = sD + (size_t)k * BS;
+  const double* gam = P.gamma + (size_t)b * vlen;
+  double r0 = valid ? gam[k * NX + i0] : 0.0, r1 = valid ? gam[k * NX + i1] : 0.0;
+  double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
+
+  // violation of the current iterate: |x_s - x_0|_1 + sum |e|_1  (sqp.py:111-115)
+  double viol_part = 0.0;
+  if (valid) {
+    if (k < N) {
+      const double* eb = P.e + ((size_t)b * N + k) * NX;
+      viol_part = fabs(eb[i0]) + fabs(eb[i1]);
+    }
+    if (k == 0) {
+      const double* xs = P.x_start + (size_t)b * NX;
+      const double* x0 = P.X + (size_t)b * nb * NX;
+      viol_part += fabs(xs[i0] - x0[i0]) + fabs(xs[i1] - x0[i1]);
+    }
+  }
+  // rows (k,i0),(k,i1) of  phi_{k-1} v_{k-1} + phi_k^T v_{k+1}  (zero rows at the ends)
+  auto offmv = [&](const double* v, double& y0, double& y1) {
+    const double* vm = v + (k > 0 ? k - 1 : 0) * NX;
+    const double* vn = v + (k < N ? k + 1 : N) * NX;
+    y0 = dot_reg<NX>(ol0, vm) + dot_reg<NX>(ou0, vn);
+    y1 = dot_reg<NX>(ol1, vm) + dot_reg<NX>(ou1, vn);
+  };
+  // z = Phi^-1 r for the current (r0, r1); three barriers
+  auto precondition = [&](double& z0, double& z1) {
+    if (valid) {
+      vr[k * NX + i0] = r0;
+      vr[k * NX + i1] = r1;
+    }
+    __syncthreads();
+    if (valid) {
+      vw[k * NX + i0] = dot_row<NX>(Dk + i0 * NX, vr + k * NX);
+      vw[k * NX + i1] = dot_row<NX>(Dk + i1 * NX, vr + k * NX);
+    }
+    __syncthreads();   // also: every read of r in vr is done
+    if (valid) {
+      double t0, t1;
+      offmv(vw, t0, t1);
+      vr[k * NX + i0] = r0 - t0;
+      vr[k * NX + i1] = r1 - t1;
+    }
+    __syncthreads();
+    z0 = valid ? dot_row<NX>(Dk + i0 * NX, vr + k * NX) : 0.0;
+    z1 = valid ? dot_row<NX>(Dk + i1 * NX, vr + k * NX) : 0.0;
+  };
+
+  int its = 0, breakdown = 0;
+  bool nan_curv = false;
+  double2 s = R.sum2(r0 * r0 + r1 * r1, viol_part);   // its barrier also publishes the D^-1 fill
+  double res = sqrt(s.x);
+  const double viol = s.y;
+  if (!(res <= P.pcg_tol)) {
+    double z0, z1;
+    precondition(z0, z1);
+    p0 = z0;
+    p1 = z1;
+    double rz = R.sum2(r0 * z0 + r1 * z1, 0.0).x;
+    const int cap = P.pcg_cap;
+    for (int it = 1; it <= cap; ++it) {
+      if (valid) {
+        vp[k * NX + i0] = p0;
+        vp[k * NX + i1] = p1;
+      }
+      __syncthreads();
+      double q0 = 0.0, q1 = 0.0;
+      if (valid) {
+        double o0, o1;
+        offmv(vp, o0, o1);
+        q0 = dot_reg<NX>(sd0, vp + k * NX) + o0;
+        q1 = dot_reg<NX>(sd1, vp + k * NX) + o1;
+      }
+      const double curv = R.sum2(p0 * q0 + p1 * q1, 0.0).x;
+      if (curv <= 0.0) {  // blocktri.py:158-161
+        breakdown = it;
+        break;
+      }
+      if (curv != curv) {  // NaN never satisfies a comparison: the reference runs to the cap
+        nan_curv = true;
+        its = cap;
+        break;
+      }
+      const double a = rz / curv;
+      l0 = l0 + a * p0;
+      l1 = l1 + a * p1;
+      r0 = r0 - a * q0;
+      r1 = r1 - a * q1;
+      double z0n, z1n;
+      precondition(z0n, z1n);
+      const double2 rr = R.sum2(r0 * z0n + r1 * z1n, r0 * r0 + r1 * r1);
+      res = sqrt(rr.y);
+      its = it;
+      if (res <= P.pcg_tol) break;
+      const double beta = rr.x / rz;
+      p0 = z0n + beta * p0;
+      p1 = z1n + beta * p1;
+      rz = rr.x;
+    }
+  }
+  if (nan_curv) l0 = l1 = nan("");
+
+  if (breakdown) {
+    if (t == 0) {
+      const int retries = si[SI_RETRIES] + 1;
+      si[SI_RETRIES] = retries;
+      if (retries > P.retry_limit) {  // sqp.py:242-247
+        record_failure(P, b, GATO_STATUS_PCG_BREAKDOWN, -1, 0, breakdown, retries);
+      } else {  // sqp.py:248
+        P.sd[b * SD_WORDS + SD_RHO] = fmin(P.sd[b * SD_WORDS + SD_RHO] * P.rho_factor, P.rho_max);
+        si[SI_SKIP_LS] = 1;
+      }
+    }
+    return;
+  }
+
+  // ---- recover_step (qpform.py:375-397); -Q^-1 A_k^T lam_{k+1} = phi_k^T lam_{k+1} from registers ----
+  __syncthreads();
+  double* vl = vp;  // lambda
+  double* vg = vr;  // q - lambda
+  double* vu = vw;  // grad_u  [N][NU]
+  const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
+  if (valid) {
+    vl[k * NX + i0] = l0;
+    vl[k * NX + i1] = l1;
+    P.lam[(size_t)b * vlen + k * NX + i0] = l0;
+    P.lam[(size_t)b * vlen + k * NX + i1] = l1;
+    vg[k * NX + i0] = g[i0] - l0;
+    vg[k * NX + i1] = g[i1] - l1;
+  }
+  __syncthreads();
+  const double* hinv = P.hinv + (size_t)b * HS;
+  if (valid && k < N) {
+    const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
+    const double* ln = vl + (k + 1) * NX;
+    for (int ju = i0; ju < NU; ju += HN) {
+      double su = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) su = fma(Bk[j * NU + ju], ln[j], su);
+      vu[k * NU + ju] = g[NX + ju] + su;
+    }
+  }
+  __syncthreads();
+  double step_part = 0.0;
+  if (valid) {
+    const double* Qk = (k < N) ? hinv : hinv + BS;
+    const double* gk = vg + k * NX;
+    double d0 = -dot_row<NX>(Qk + i0 * NX, gk);
+    double d1 = -dot_row<NX>(Qk + i1 * NX, gk);
+    if (k < N) {
+      d0 += dot_reg<NX>(ou0, vl + (k + 1) * NX);
+      d1 += dot_reg<NX>(ou1, vl + (k + 1) * NX);
+    }
+    double* dX = P.dX + ((size_t)b * nb + k) * NX;
+    dX[i0] = d0;
+    dX[i1] = d1;
+    step_part = nanmax(fabs(d0), fabs(d1));
+    if (k < N) {
+      const double* Ri = hinv + 2 * BS;
+      const double* gu = vu + k * NU;
+      double* dU = P.dU + ((size_t)b * N + k) * NU;
+      for (int ju = i0; ju < NU; ju += HN) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
+        dU[ju] = -acc;
+        step_part = nanmax(step_part, fabs(acc));
+      }
+    }
+  }
+  const double step_inf = R.max1(step_part);
+  if (t == 0) {
+    si[SI_RETRIES] = 0;
+    si[SI_PCG_ITS] = its;
+    P.sd[b * SD_WORDS + SD_STEP_INF] = step_inf;
+    P.sd[b * SD_WORDS + SD_VIOL] = viol;
+    const int it = si[SI_IT];
+    P.pcg_iters[(size_t)b * P.max_it + it] = its;
+    const bool tol_mode = P.step_tol == P.step_tol;  // NaN => None
+    if (tol_mode && step_inf <= P.step_tol && viol <= P.feas_tol) {  // sqp.py:256-272
+      double* tr = P.trace + ((size_t)b * P.max_it + it) * GATO_TRACE_WORDS;
+      tr[GATO_TRACE_MERIT] = P.sd[b * SD_WORDS + SD_MERIT];
+      tr[GATO_TRACE_CONSTRAINT_L1] = viol;
+      tr[GATO_TRACE_ALPHA] = nan("");
+      tr[GATO_TRACE_RHO] = P.sd[b * SD_WORDS + SD_RHO];
+      tr[GATO_TRACE_PCG_ITERATIONS] = (double)its;
+      tr[GATO_TRACE_ACCEPTED] = 0.0;
+      tr[GATO_TRACE_STEP_INF_NORM] = step_inf;
+      tr[GATO_TRACE_ITERATION] = (double)it;
+      int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
+      info[GATO_INFO_N_RECORDS] = it + 1;
+      info[GATO_INFO_CONVERGED] = 1;
+      si[SI_ACTIVE] = 0;
+      si[SI_SKIP_LS] = si[SI_MERIT_VALID] ? 1 : 2;
+    } else {
+      si[SI_SKIP_LS] = 0;
+    }
+  }
+}
+
+// -----------------------------------------------------------------------------------------
 // k_linesearch: merit of every candidate (sqp.py:132-166).  grid (C, M), one thread per stage
 // knot: candidate point (X + a dX, U + a dU), one RK4 prediction, |defect|_1, quadratic cost
 // with the undamped weights; fixed-tree reduction over knots.  Non-finite candidates -> +inf.
