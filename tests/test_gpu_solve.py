@@ -140,3 +140,53 @@ def test_loop_modes_agree_bitwise():
     for res, _ in outs[1:]:
         assert np.array_equal(res.X, base.X) and np.array_equal(res.U, base.U)
         assert np.array_equal(res.trace, base.trace, equal_nan=True) and np.array_equal(res.info, base.info)
+
+
+@pytest.mark.parametrize("model_name,N", [("di7", 128), ("iiwa14", 128), ("iiwa14", 48), ("pendulum", 200)])
+def test_long_horizons_match_the_oracle(model_name, N):
+    """BASELINE.json sweep reaches N=128: beyond N~66 (n=14) the PCG kernel reads the matrix record
+    from global memory instead of shared memory; N=48 exercises the fat-thread shared-memory path
+    (the golden cases stop at N=32 for n=14)."""
+    from oracle import trajopt_np as orc
+    rng = np.random.default_rng(77)
+    if model_name == "iiwa14":
+        batch = workloads.iiwa14_reach_arrays(2, N, seed=5)
+        model, h, iters = gb.Iiwa14(), 0.02, 2
+    elif model_name == "di7":
+        model, h, iters = gb.DoubleIntegrator(dims=7), 0.05, 3
+        n, m = 14, 7
+        from paper_2510_07625_b200.engine import PackedBatch
+        M = 2
+        W = rng.standard_normal((M, n, n))
+        Q = W @ W.transpose(0, 2, 1) / n + 0.5 * np.eye(n)
+        V = rng.standard_normal((M, m, m))
+        Rm = V @ V.transpose(0, 2, 1) / m + 0.5 * np.eye(m)
+        batch = PackedBatch(x_start=0.3 * rng.standard_normal((M, n)), goal=np.repeat(0.5 * rng.standard_normal((M, 1, n)), N + 1, 1),
+                            Q=Q, R=Rm, QN=3.0 * Q, force=np.repeat(0.2 * rng.standard_normal((M, 1, m)), N, 1),
+                            rho_init=np.full(M, 1e-4), X=0.1 * rng.standard_normal((M, N + 1, n)),
+                            U=0.1 * rng.standard_normal((M, N, m)))
+    else:
+        model, h, iters = gb.Pendulum(), 0.05, 4
+        from paper_2510_07625_b200.engine import PackedBatch
+        M = 2
+        batch = PackedBatch(x_start=np.zeros((M, 2)), goal=np.tile(np.array([np.pi, 0.0]), (M, N + 1, 1)),
+                            Q=np.tile(np.diag([1.0, 0.1]), (M, 1, 1)), R=np.full((M, 1, 1), 0.01),
+                            QN=np.tile(np.diag([100.0, 10.0]), (M, 1, 1)), force=np.zeros((M, N, 1)),
+                            rho_init=np.array([1e-4, 1e-2]), X=np.zeros((M, N + 1, 2)), U=np.zeros((M, N, 1)))
+    st = gb.SolverSettings(max_sqp_iterations=iters, step_tolerance=None, pcg=gb.PcgSettings(tolerance=1e-6))
+    eng = gb.BatchEngine(model, batch.size, N, h, st)
+    try:
+        res = eng.solve(batch)
+    finally:
+        eng.close()
+    omodel = orc.model_from_descriptor(model)
+    for b in range(batch.size):
+        ost = orc.Settings(max_sqp_iterations=iters, pcg_tolerance=1e-6, step_tolerance=None,
+                           rho_init=float(batch.rho_init[b]))
+        p = orc.Problem(omodel, batch.Q[b], batch.R[b], batch.QN[b], batch.goal[b], N, h, batch.x_start[b],
+                        batch.force[b])
+        ref = orc.solve(p, batch.X[b], batch.U[b], ost)
+        assert rel_inf(res.X[b], ref.X) <= TRAJ_TOL and rel_inf(res.U[b], ref.U) <= TRAJ_TOL
+        pcg_ref = np.array([r.pcg_iterations for r in ref.trace])
+        assert np.max(np.abs(res.trace[b, :iters, 4] - pcg_ref)) <= 1
+        assert int(res.info[b, 0]) == len(ref.trace)
