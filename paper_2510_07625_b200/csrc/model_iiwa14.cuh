@@ -183,9 +183,10 @@ struct Stage {
   V3 w[NJ], v[NJ];      // link velocities
   V3 awp[NJ], avp[NJ];  // parent acceleration transformed into the link frame (X_i a_parent)
   V3 N[NJ], F[NJ];      // accumulated link forces of ID(q, qd, qdd)
-  double Minv[28];      // lower triangle of M^-1, row-major packed
+  double L[28];         // lower Cholesky factor of M(q), row-major packed
+  double invd[NJ];      // reciprocals of its diagonal
 };
-static_assert(sizeof(Stage) == 175 * 8, "Stage layout");
+static_assert(sizeof(Stage) == 182 * 8, "Stage layout");
 
 __device__ __forceinline__ int tri(int i, int j) { return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i; }
 
@@ -353,18 +354,17 @@ __device__ __forceinline__ void mass_matrix(const double* s, const double* c, do
   });
 }
 
-// In-place lower Cholesky of a packed 7x7; returns false if a pivot is not positive.
-__device__ __forceinline__ bool chol7(double* L) {
-  bool ok = true;
+// In-place lower Cholesky of a packed 7x7 (M(q) is SPD); invd receives 1 / L_ii.
+__device__ __forceinline__ void chol7(double* L, double* invd) {
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     double d = L[tri(j, j)];
 #pragma unroll
     for (int k = 0; k < j; ++k) d = fma(-L[tri(j, k)], L[tri(j, k)], d);
-    ok = ok && (d > 0.0);
     const double r = sqrt(d);
     const double ir = 1.0 / r;
     L[tri(j, j)] = r;
+    invd[j] = ir;
 #pragma unroll
     for (int i = j + 1; i < NJ; ++i) {
       double t = L[tri(i, j)];
@@ -373,31 +373,27 @@ __device__ __forceinline__ bool chol7(double* L) {
       L[tri(i, j)] = t * ir;
     }
   }
-  return ok;
 }
-// solve L L^T x = b in place (L packed lower)
-__device__ __forceinline__ void chol7_solve(const double* L, double* b) {
+// solve L L^T x = b in place (L packed lower, invd = 1 / diag(L))
+__device__ __forceinline__ void chol7_solve(const double* L, const double* invd, double* b) {
 #pragma unroll
   for (int i = 0; i < NJ; ++i) {
     double t = b[i];
 #pragma unroll
     for (int k = 0; k < i; ++k) t = fma(-L[tri(i, k)], b[k], t);
-    b[i] = t / L[tri(i, i)];
+    b[i] = t * invd[i];
   }
 #pragma unroll
   for (int i = NJ - 1; i >= 0; --i) {
     double t = b[i];
 #pragma unroll
     for (int k = i + 1; k < NJ; ++k) t = fma(-L[tri(k, i)], b[k], t);
-    b[i] = t / L[tri(i, i)];
+    b[i] = t * invd[i];
   }
 }
 
-// Forward dynamics, single thread: xdot = f(x, u, fw).  With KEEP the stage data for the
-// tangent passes (kinematics, forces of ID(q,qd,qdd), M^-1) is written to *st.
-template <bool KEEP>
-__device__ __forceinline__ void forward_dynamics(const double* x, const double* u, const double* fw3,
-                                                 double* xdot, Stage* st) {
+// Forward dynamics, single thread: xdot = f(x, u, fw)  (line search, RK4 step operator).
+__device__ __forceinline__ void forward_dynamics(const double* x, const double* u, const double* fw3, double* xdot) {
   double s[NJ], c[NJ], qd[NJ], tau[NJ];
 #pragma unroll
   for (int i = 0; i < NJ; ++i) {
@@ -406,37 +402,17 @@ __device__ __forceinline__ void forward_dynamics(const double* x, const double* 
   }
   const V3 fw = {fw3[0], fw3[1], fw3[2]};
   newton_euler<false, true>(s, c, qd, nullptr, fw, tau, nullptr);
-  double L[28];
+  double L[28], invd[NJ];
   mass_matrix(s, c, L);
-  chol7(L);
+  chol7(L, invd);
   double qdd[NJ];
 #pragma unroll
   for (int i = 0; i < NJ; ++i) qdd[i] = u[i] - tau[i];
-  chol7_solve(L, qdd);
+  chol7_solve(L, invd, qdd);
 #pragma unroll
   for (int i = 0; i < NJ; ++i) {
     xdot[i] = qd[i];
     xdot[NJ + i] = qdd[i];
-  }
-  if constexpr (KEEP) {
-#pragma unroll
-    for (int i = 0; i < NJ; ++i) {
-      st->s[i] = s[i];
-      st->c[i] = c[i];
-      st->qd[i] = qd[i];
-    }
-    // M^-1 column by column (symmetric: keep the lower triangle)
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      double e[NJ];
-#pragma unroll
-      for (int i = 0; i < NJ; ++i) e[i] = (i == j) ? 1.0 : 0.0;
-      chol7_solve(L, e);
-#pragma unroll
-      for (int i = j; i < NJ; ++i) st->Minv[tri(i, j)] = e[i];
-    }
-    double tau2[NJ];
-    newton_euler<true, false>(s, c, qd, qdd, fw, tau2, st);
   }
 }
 
@@ -504,13 +480,15 @@ __device__ __forceinline__ void tangent(const Stage* __restrict__ st, const doub
       dF[I - 1] = dF[I - 1] + f_up;
     }
   });
+  // d qdd = M^-1 (du - d tau) through the stage's Cholesky factor
+  double rhs[NJ];
+#pragma unroll
+  for (int i = 0; i < NJ; ++i) rhs[i] = ((i == du_idx) ? 1.0 : 0.0) - dtau[i];
+  chol7_solve(st->L, st->invd, rhs);
 #pragma unroll
   for (int i = 0; i < NJ; ++i) {
     dxdot[i] = dx[NJ + i];
-    double acc = (du_idx >= 0) ? st->Minv[tri(i, du_idx)] : 0.0;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) acc = fma(-st->Minv[tri(i, j)], dtau[j], acc);
-    dxdot[NJ + i] = acc;
+    dxdot[NJ + i] = rhs[i];
   }
 }
 

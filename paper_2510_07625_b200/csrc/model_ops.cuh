@@ -50,7 +50,8 @@ cudaError_t launch_linearize(const RowView& V, const ModelParams& mp, double h, 
     k_linearize_simple<Mdl><<<(unsigned)((rows + threads - 1) / threads), threads, 0, s>>>(V, mp, h, rows, A, B, e);
   } else {
     iiwa::Stage* stages = static_cast<iiwa::Stage*>(scratch);
-    k_lin_primal_iiwa<0><<<(unsigned)((rows + 63) / 64), 64, 0, s>>>(V, h, rows, stages, e);
+    k_lin_primal_iiwa<0><<<(unsigned)((rows + linp::KNOTS - 1) / linp::KNOTS), 96, 4 * sizeof(linp::Slot), s>>>(
+        V, h, rows, stages, e);
     k_lin_tangent_iiwa<0><<<(unsigned)((rows + kLinKnotsPerCta - 1) / kLinKnotsPerCta), 128, 0, s>>>(V, h, rows, stages,
                                                                                                    A, B);
   }
@@ -148,6 +149,11 @@ template <class Mdl>
 cudaError_t prepare_attrs(const SolveParams& P) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU;
   cudaError_t err;
+  if constexpr (!Mdl::ANALYTIC_JAC) {
+    err = cudaFuncSetAttribute(k_lin_primal_iiwa<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(4 * sizeof(linp::Slot)));
+    if (err != cudaSuccess) return err;
+  }
   err = cudaFuncSetAttribute(k_schur<NX, NU, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(4 * sizeof(SchurSmem<NX, NU>)));
   if (err != cudaSuccess) return err;

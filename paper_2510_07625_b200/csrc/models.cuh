@@ -235,7 +235,7 @@ struct Iiwa14Model {
   static constexpr bool ANALYTIC_JAC = false;
   __device__ static __forceinline__ void deriv(const ModelParams&, const double* x, const double* u, const double* f,
                                                double* xdot) {
-    iiwa::forward_dynamics<false>(x, u, f, xdot, nullptr);
+    iiwa::forward_dynamics(x, u, f, xdot);
   }
 };
 

@@ -278,42 +278,164 @@ __global__ void k_linearize_simple(RowView V, ModelParams mp, double h, int64_t 
 //                     n x n x n product and no cross-thread traffic.  The 21 direction threads of
 //                     a knot read the same stage record (L1 broadcast).
 // -----------------------------------------------------------------------------------------
+// k_lin_primal_iiwa: 32 knots per CTA (lane = knot), three warps with three roles that pipeline
+// through the four RK4 stages (the serial chain of one stage is what bounds this kernel):
+//   warp 0  sincos, bias torques (RNEA at qdd = 0), solve with the stage's Cholesky factor -> qdd,
+//           RK4 bookkeeping (next stage point, defect e_k)
+//   warp 1  sincos, composite-rigid-body mass matrix, Cholesky factor L (-> stage record)
+//   warp 2  sincos, RNEA at the solved qdd, link quantities the tangent passes need (-> stage record)
+// Hand-offs go through per-stage shared-memory slots and per-stage named barriers, so no slot or
+// barrier is ever reused.
+namespace linp {
+constexpr int KNOTS = 32;
+struct Slot {             // one RK4 stage of one CTA
+  double L[28][KNOTS];
+  double invd[7][KNOTS];
+  double qdd[7][KNOTS];
+  double xnext[14][KNOTS];   // stage point of the NEXT stage
+};
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+}  // namespace linp
+
 template <int UNUSED = 0>
-__global__ void __launch_bounds__(64) k_lin_primal_iiwa(RowView V, double h, int64_t rows,
+__global__ void __launch_bounds__(96) k_lin_primal_iiwa(RowView V, double h, int64_t rows,
                                                         iiwa::Stage* __restrict__ stages, double* __restrict__ e) {
-  constexpr int NX = 14, NU = 7, NF = 3;
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  const int64_t b = r / V.N, k = r % V.N;
-  if (V.si && !V.si[b * SI_WORDS + SI_ACTIVE]) return;
-  const double* xg = V.X + (b * (V.N + 1) + k) * NX;
-  double x[NX], u[NU], f[NF], kk[NX], xs[NX], ksum[NX];
-#pragma unroll
-  for (int i = 0; i < NX; ++i) {
-    x[i] = xg[i];
-    xs[i] = x[i];
-    ksum[i] = 0.0;
+  constexpr int NX = 14, NU = 7, NF = 3, NJ = 7;
+  extern __shared__ __align__(16) unsigned char linp_smem[];
+  linp::Slot* slots = reinterpret_cast<linp::Slot*>(linp_smem);
+  const int role = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * linp::KNOTS + lane;
+  bool valid = r < rows;
+  int64_t b = 0, k = 0;
+  if (valid) {
+    b = r / V.N;
+    k = r % V.N;
+    if (V.si && !V.si[b * SI_WORDS + SI_ACTIVE]) valid = false;
   }
+  // invalid lanes run on a harmless dummy state so that every warp reaches every barrier
+  const double* xg = valid ? V.X + (b * (V.N + 1) + k) * NX : nullptr;
+  double x[NX], f[NF];
 #pragma unroll
-  for (int i = 0; i < NU; ++i) u[i] = V.U[r * NU + i];
+  for (int i = 0; i < NX; ++i) x[i] = valid ? xg[i] : 0.0;
 #pragma unroll
-  for (int i = 0; i < NF; ++i) f[i] = V.F[r * NF + i];
-  iiwa::Stage* st = stages + r * 4;
-#pragma unroll 1
-  for (int s = 0; s < 4; ++s) {
-    iiwa::forward_dynamics<true>(xs, u, f, kk, st + s);
-    const double wgt = (s == 0 || s == 3) ? 1.0 : 2.0;
-    const double lead = (s == 2) ? h : 0.5 * h;   // offset of the NEXT stage point
+  for (int i = 0; i < NF; ++i) f[i] = valid ? V.F[r * NF + i] : 0.0;
+  const iiwa::V3 fw = {f[0], f[1], f[2]};
+  iiwa::Stage* st = stages + (valid ? r : 0) * 4;
+  // barrier ids: 1..4 "L of stage s ready" (warps 0+1), 5..8 "qdd of stage s and next point ready" (all)
+  if (role == 0) {
+    double u[NU], xs[NX], ksum[NX];
+#pragma unroll
+    for (int i = 0; i < NU; ++i) u[i] = valid ? V.U[r * NU + i] : 0.0;
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
-      ksum[i] = ksum[i] + wgt * kk[i];
-      xs[i] = x[i] + lead * kk[i];
+      xs[i] = x[i];
+      ksum[i] = 0.0;
     }
-  }
-  if (e) {
-    const double* xn = xg + NX;
+#pragma unroll 1
+    for (int s = 0; s < 4; ++s) {
+      double sn[NJ], cs[NJ], tau[NJ], L[28], invd[NJ], qdd[NJ];
 #pragma unroll
-    for (int i = 0; i < NX; ++i) e[r * NX + i] = (x[i] + (h / 6.0) * ksum[i]) - xn[i];
+      for (int i = 0; i < NJ; ++i) sincos(xs[i], &sn[i], &cs[i]);
+      iiwa::newton_euler<false, true>(sn, cs, xs + NJ, nullptr, fw, tau, nullptr);
+      linp::bar_sync(1 + s, 64);
+      linp::Slot& sl = slots[s];
+#pragma unroll
+      for (int i = 0; i < 28; ++i) L[i] = sl.L[i][lane];
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) {
+        invd[i] = sl.invd[i][lane];
+        qdd[i] = u[i] - tau[i];
+      }
+      iiwa::chol7_solve(L, invd, qdd);
+      const double wgt = (s == 0 || s == 3) ? 1.0 : 2.0;
+      const double lead = (s == 2) ? h : 0.5 * h;   // offset of the NEXT stage point
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) {
+        sl.qdd[i][lane] = qdd[i];
+        ksum[i] = ksum[i] + wgt * xs[NJ + i];
+        ksum[NJ + i] = ksum[NJ + i] + wgt * qdd[i];
+      }
+      double xn[NX];
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) {
+        xn[i] = x[i] + lead * xs[NJ + i];
+        xn[NJ + i] = x[NJ + i] + lead * qdd[i];
+      }
+#pragma unroll
+      for (int i = 0; i < NX; ++i) {
+        xs[i] = xn[i];
+        sl.xnext[i][lane] = xn[i];
+      }
+      __threadfence_block();
+      linp::bar_arrive(5 + s, 96);
+    }
+    if (e && valid) {
+      const double* xnk = xg + NX;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) e[r * NX + i] = (x[i] + (h / 6.0) * ksum[i]) - xnk[i];
+    }
+  } else if (role == 1) {
+    double q[NJ];
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) q[i] = x[i];
+#pragma unroll 1
+    for (int s = 0; s < 4; ++s) {
+      if (s > 0) {
+        linp::bar_sync(5 + s - 1, 96);
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) q[i] = slots[s - 1].xnext[i][lane];
+      }
+      double sn[NJ], cs[NJ], L[28], invd[NJ];
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) sincos(q[i], &sn[i], &cs[i]);
+      iiwa::mass_matrix(sn, cs, L);
+      iiwa::chol7(L, invd);
+      linp::Slot& sl = slots[s];
+#pragma unroll
+      for (int i = 0; i < 28; ++i) sl.L[i][lane] = L[i];
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) sl.invd[i][lane] = invd[i];
+      __threadfence_block();
+      linp::bar_sync(1 + s, 64);
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 28; ++i) st[s].L[i] = L[i];
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) st[s].invd[i] = invd[i];
+      }
+    }
+    linp::bar_sync(5 + 3, 96);
+  } else {
+    double xs[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) xs[i] = x[i];
+#pragma unroll 1
+    for (int s = 0; s < 4; ++s) {
+      double sn[NJ], cs[NJ], qdd[NJ], tau[NJ];
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) sincos(xs[i], &sn[i], &cs[i]);   // before the wait: independent of qdd
+      linp::bar_sync(5 + s, 96);
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) qdd[i] = slots[s].qdd[i][lane];
+      // invalid lanes write their (dummy) record to a scratch copy of knot 0's slot: harmless only if
+      // nobody reads it, so give them a private dump instead
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) {
+          st[s].s[i] = sn[i];
+          st[s].c[i] = cs[i];
+          st[s].qd[i] = xs[NJ + i];
+        }
+        iiwa::newton_euler<true, false>(sn, cs, xs + NJ, qdd, fw, tau, st + s);
+      }
+#pragma unroll
+      for (int i = 0; i < NX; ++i) xs[i] = slots[s].xnext[i][lane];
+    }
   }
 }
 

@@ -1,0 +1,38 @@
+"""Small solves of every kernel variant, for compute-sanitizer (memcheck / racecheck / synccheck).
+    compute-sanitizer --tool racecheck python scripts/sanitize_small.py"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import paper_2510_07625_b200 as gb  # noqa: E402
+from paper_2510_07625_b200 import workloads  # noqa: E402
+from conftest import load_golden, product_problem, product_settings  # noqa: E402
+
+# iiwa14: real-time PCG (N=8), fat-thread PCG T=1 (N=40 > 35), global-memory PCG (N=70)
+for N, iters in ((8, 2), (40, 1), (70, 1)):
+    batch = workloads.iiwa14_reach_arrays(3, N)
+    eng = gb.BatchEngine(gb.Iiwa14(), 3, N, 0.02, workloads.fixed_budget_settings(iters), loop_mode=3)
+    res = eng.solve(batch)
+    eng.shift_warm_start()
+    eng.stream.synchronize()
+    print("iiwa14 N", N, "status", res.info[:, 2].tolist(), "pcg", res.trace[:, 0, 4].tolist())
+    eng.close()
+# the reference's analytic models (k_linearize_simple, small block sizes)
+for name in ("pendulum_n8", "cartpole_n8", "twolink_n8", "di7_n8"):
+    g = load_golden(name)
+    r = gb.sqp_solve(product_problem(g), g["X0"], g["U0"], product_settings(g))
+    print(name, len(r.trace), float(np.max(np.abs(r.X - g["X"]))))
+# operators
+rng = np.random.default_rng(0)
+X, U, F = rng.standard_normal((5, 14)), rng.standard_normal((5, 7)), rng.standard_normal((5, 3))
+gb.step_many(gb.Iiwa14(), X, U, 0.02, F)
+gb.step_jacobians_many(gb.Iiwa14(), X, U, 0.02, F)
+d = np.tile(np.eye(3) * 4.0, (2, 5, 1, 1))
+o = 0.1 * rng.standard_normal((2, 4, 3, 3))
+gb.pcg_batched(d, o, rng.standard_normal((2, 15)), np.tile(np.eye(3) / 4.0, (2, 5, 1, 1)), np.zeros((2, 4, 3, 3)), 1e-10)
+print("done")
