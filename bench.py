@@ -255,10 +255,18 @@ def run_gpu_arm(args, w, rank, local_rank, world):
     from paper_2510_07625_b200 import _lib, sharding, workloads
     from paper_2510_07625_b200.engine import PackedBatch, measure_fp64_peak
 
+    # GATO_DIST_BACKEND=gloo lets the multi-rank path be exercised on a box with fewer GPUs than
+    # ranks (ranks wrap around the visible devices, collectives go through host memory)
+    backend = os.environ.get("GATO_DIST_BACKEND", "nccl")
+    local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
+    coll_device = device if backend == "nccl" else torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
 
     M, N, h, K_sqp = w["M"], w["N"], w["h"], w["sqp"]
     settings = workloads.fixed_budget_settings(K_sqp)
@@ -374,10 +382,10 @@ def run_gpu_arm(args, w, rank, local_rank, world):
     P_prof = prof_res.trace[:, :K_sqp, _lib.TRACE_PCG_ITERATIONS]
 
     # ---- max over ranks ----
-    agg = torch.tensor([dev_ms, e2e_s, wall1 - wall0], dtype=torch.float64, device=device)
+    agg = torch.tensor([dev_ms, e2e_s, wall1 - wall0], dtype=torch.float64, device=coll_device)
     if world > 1:
         dist.all_reduce(agg, op=dist.ReduceOp.MAX)
-        gathered = sharding.gather_results(res_last, [M] * world, rank, world, device=device)
+        gathered = sharding.gather_results(res_last, [M] * world, rank, world, device=coll_device)
     else:
         gathered = res_last
     dev_ms_max, e2e_s_max, wall_max = (float(v) for v in agg.tolist())

@@ -52,8 +52,14 @@ cudaError_t launch_linearize(const RowView& V, const ModelParams& mp, double h, 
     iiwa::Stage* stages = static_cast<iiwa::Stage*>(scratch);
     k_lin_primal_iiwa<0><<<(unsigned)((rows + linp::KNOTS - 1) / linp::KNOTS), 96, 4 * sizeof(linp::Slot), s>>>(
         V, h, rows, stages, e);
-    k_lin_tangent_iiwa<0><<<(unsigned)((rows + kLinKnotsPerCta - 1) / kLinKnotsPerCta), 128, 0, s>>>(V, h, rows, stages,
-                                                                                                   A, B);
+    {
+      static int minb = 0;
+      if (!minb) minb = env_int("GATO_TAN_MINB", 2);
+      const unsigned grid = (unsigned)((rows + kLinKnotsPerCta - 1) / kLinKnotsPerCta);
+      if (minb == 3) k_lin_tangent_iiwa<3><<<grid, 128, 0, s>>>(V, h, rows, stages, A, B);
+      else if (minb == 4) k_lin_tangent_iiwa<4><<<grid, 128, 0, s>>>(V, h, rows, stages, A, B);
+      else k_lin_tangent_iiwa<2><<<grid, 128, 0, s>>>(V, h, rows, stages, A, B);
+    }
   }
   return cudaGetLastError();
 }
@@ -128,7 +134,11 @@ cudaError_t launch_linesearch(const SolveParams& P, cudaStream_t s) {
   int threads = ((P.N + 31) / 32) * 32;
   if (threads > 128) threads = 128;
   dim3 grid(P.C + 1, P.M);   // C step-length candidates + the alpha = 0 candidate of the first iteration
-  k_linesearch<Mdl><<<grid, threads, 0, s>>>(P);
+  static int minb = 0;
+  if (!minb) minb = env_int("GATO_LS_MINB", 1);
+  if (minb == 3) k_linesearch<Mdl, 3><<<grid, threads, 0, s>>>(P);
+  else if (minb == 4) k_linesearch<Mdl, 4><<<grid, threads, 0, s>>>(P);
+  else k_linesearch<Mdl, 1><<<grid, threads, 0, s>>>(P);
   return cudaGetLastError();
 }
 
