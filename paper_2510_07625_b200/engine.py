@@ -125,16 +125,32 @@ class BatchEngine:
             "X": (M, N + 1, n), "U": (M, N, m),
         }
         max_it = settings.max_sqp_iterations
+        # One device arena and one pinned mirror, laid out so that every transfer of the hot loop is
+        # ONE copy:  [x_start goal force | Q R QN rho_init | X U | trace info]
+        #   per-step MPC inputs = the first three fields, full upload = everything up to U,
+        #   download = X .. info.
+        self.layout = ("x_start", "goal", "force", "Q", "R", "QN", "rho_init", "X", "U", "trace", "info")
+        shapes = dict(self.shapes)
+        shapes["trace"] = (M, max_it, _lib.TRACE_WORDS)
+        info_doubles = (M * _lib.INFO_WORDS + 1) // 2          # int32 words stored in 8-byte slots
+        self.offsets, off = {}, 0
+        for name in self.layout:
+            count = info_doubles if name == "info" else int(np.prod(shapes[name]))
+            self.offsets[name] = (off, count)
+            off += count + (count & 1)                         # keep every field 16-byte aligned
+        self.arena_doubles = off
         with torch.cuda.device(self.device):
-            self.dev = {k: torch.zeros(s, dtype=torch.float64, device=self.device)
-                        for k, s in self.shapes.items()}
-            self.dev["trace"] = torch.zeros((M, max_it, _lib.TRACE_WORDS), dtype=torch.float64,
-                                            device=self.device)
-            self.dev["info"] = torch.zeros((M, _lib.INFO_WORDS), dtype=torch.int32, device=self.device)
-            self.pin_in = {k: torch.zeros(s, dtype=torch.float64).pin_memory()
-                           for k, s in self.shapes.items()}
-            self.pin_out = {k: torch.zeros_like(self.dev[k], device="cpu").pin_memory()
-                            for k in ("X", "U", "trace", "info")}
+            self.arena = torch.zeros(off, dtype=torch.float64, device=self.device)
+            self.pinned = torch.zeros(off, dtype=torch.float64).pin_memory()
+
+            def view(buf, name):
+                o, c = self.offsets[name]
+                if name == "info":
+                    return buf[o:o + c].view(torch.int32)[:M * _lib.INFO_WORDS].view(M, _lib.INFO_WORDS)
+                return buf[o:o + c].view(shapes[name])
+            self.dev = {name: view(self.arena, name) for name in self.layout}
+            self.pin = {name: view(self.pinned, name) for name in self.layout}
+            self.pin_np = {name: t.numpy() for name, t in self.pin.items()}
             self.stream = torch.cuda.Stream(device=self.device)
             cfg = make_config(model, M, N, timestep, settings, loop_mode)
             handle = C.c_void_p()
@@ -173,16 +189,28 @@ class BatchEngine:
         return int(self.lib.gato_loop_mode(self.handle))
 
     # -- staged steps (all asynchronous on self.stream) ---------------------------- #
+    def _span(self, first: str, last: str) -> slice:
+        return slice(self.offsets[first][0], self.offsets[last][0] + self.offsets[last][1])
+
     def upload(self, batch: PackedBatch, fields=INPUT_FIELDS):
-        """Host -> pinned -> device for the named inputs."""
+        """Host -> pinned -> device for the named inputs: one contiguous copy when the fields are
+        adjacent in the arena (the per-step MPC inputs x_start, goal, force; or everything)."""
         torch = self.torch
+        for name in fields:
+            src = getattr(batch, name)
+            if src.shape != self.shapes[name]:
+                raise ValueError(f"{name}: expected shape {self.shapes[name]}, got {src.shape}")
+            self.pin_np[name][...] = src
+        order = [n for n in self.layout if n in fields]
         with torch.cuda.stream(self.stream):
-            for name in fields:
-                src = np.ascontiguousarray(getattr(batch, name), dtype=np.float64)
-                if src.shape != self.shapes[name]:
-                    raise ValueError(f"{name}: expected shape {self.shapes[name]}, got {src.shape}")
-                self.pin_in[name].numpy()[...] = src
-                self.dev[name].copy_(self.pin_in[name], non_blocking=True)
+            i = 0
+            while i < len(order):          # maximal runs of adjacent fields
+                j = i
+                while j + 1 < len(order) and self.layout.index(order[j + 1]) == self.layout.index(order[j]) + 1:
+                    j += 1
+                span = self._span(order[i], order[j])
+                self.arena[span].copy_(self.pinned[span], non_blocking=True)
+                i = j + 1
 
     def launch(self):
         """gato_solve on the engine stream; loops on the device until every solve terminated."""
@@ -203,16 +231,16 @@ class BatchEngine:
             guard -= 1
 
     def download(self) -> PackedResult:
+        """Device -> pinned -> host for X, U, trace, info: one copy."""
         torch = self.torch
+        span = self._span("X", "info")
         with torch.cuda.stream(self.stream):
-            for name in ("X", "U", "trace", "info"):
-                self.pin_out[name].copy_(self.dev[name], non_blocking=True)
+            self.pinned[span].copy_(self.arena[span], non_blocking=True)
         self.stream.synchronize()
         ms = C.c_float(0.0)
         self._check(self.lib.gato_last_solve_ms(self.handle, C.byref(ms)), "gato_last_solve_ms")
-        return PackedResult(self.pin_out["X"].numpy().copy(), self.pin_out["U"].numpy().copy(),
-                            self.pin_out["trace"].numpy().copy(), self.pin_out["info"].numpy().copy(),
-                            float(ms.value))
+        return PackedResult(self.pin_np["X"].copy(), self.pin_np["U"].copy(), self.pin_np["trace"].copy(),
+                            self.pin_np["info"].copy(), float(ms.value))
 
     def solve(self, batch: PackedBatch) -> PackedResult:
         """The end-to-end call: host inputs in, host results out."""

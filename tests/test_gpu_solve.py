@@ -190,3 +190,40 @@ def test_long_horizons_match_the_oracle(model_name, N):
         pcg_ref = np.array([r.pcg_iterations for r in ref.trace])
         assert np.max(np.abs(res.trace[b, :iters, 4] - pcg_ref)) <= 1
         assert int(res.info[b, 0]) == len(ref.trace)
+
+
+def _random_problem(rng, model):
+    """Same recipe as the reference's oracles.random_problem (oracles.py:136-163): dense random
+    SPD weights, random goal, timestep, start state, constant force and an infeasible random
+    initial trajectory."""
+    def spd(n, scale=1.0):
+        W = rng.standard_normal((n, n))
+        return scale * (W @ W.T / n + 0.5 * np.eye(n))
+    N = int(rng.choice([4, 8]))
+    n, m = model.state_dim, model.control_dim
+    cost = gb.CostSpec(Q=spd(n), R=spd(m), QN=spd(n, 3.0), goal=0.5 * rng.standard_normal(n))
+    problem = gb.ProblemSpec(model=model, cost=cost, horizon=N, timestep=float(rng.uniform(0.02, 0.08)),
+                             x_start=0.3 * rng.standard_normal(n),
+                             force=gb.ExternalForce.constant(0.2 * rng.standard_normal(model.force_dim)))
+    return problem, 0.4 * rng.standard_normal((N + 1, n)), 0.4 * rng.standard_normal((N, m))
+
+
+@pytest.mark.parametrize("seed", range(15))
+def test_random_instances_over_the_model_pool_match_the_oracle(seed):
+    """The reference's verification-suite pattern (oracles.schur_kkt_suite, acceptance #1): random
+    instances cycling through the model pool, default tolerance-mode settings."""
+    from oracle import trajopt_np as orc
+    pool = [gb.DoubleIntegrator(dims=1), gb.Pendulum(), gb.Cartpole(), gb.TwoLinkArm(), gb.DoubleIntegrator(dims=2)]
+    rng = np.random.default_rng(2024 + seed)
+    problem, X, U = _random_problem(rng, pool[seed % len(pool)])
+    st = gb.SolverSettings(max_sqp_iterations=8)
+    res = gb.sqp_solve(problem, X, U, st)
+    ref = orc.solve(orc.Problem.from_spec(problem), X, U, orc.Settings(max_sqp_iterations=8))
+    assert rel_inf(res.X, ref.X) <= TRAJ_TOL and rel_inf(res.U, ref.U) <= TRAJ_TOL
+    assert len(res.trace) == len(ref.trace) and res.converged == ref.converged
+    got, want = trace_rows(res), trace_rows(ref)
+    flip = _first_decision_flip(got, want)
+    if flip < len(want):
+        assert _on_plateau(want, flip)
+    upto = min(len(want), flip + 1)
+    assert np.max(np.abs(got[:upto, 5] - want[:upto, 5])) <= 1
