@@ -253,9 +253,11 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   ALLOC(hinv, M * hinv_stride(nx, nu));
   ALLOC(Sdiag, M * nb * nx * nx);
   ALLOC(Soff, M * N * nx * nx);
-  ALLOC(Dinv, M * nb * (nx * (nx + 1) / 2));
+  ALLOC(Linv, M * nb * (nx * (nx + 1) / 2));
+  ALLOC(Lfac, M * nb * (nx * (nx + 1) / 2));
   ALLOC(pmats, M * (int64_t)h->ops.pcg_mat_doubles((int)N));
   ALLOC(gamma, M * nb * nx);
+  ALLOC(gammaw, M * nb * nx);
   ALLOC(lam, M * nb * nx);
   ALLOC(dX, M * nb * nx);
   ALLOC(dU, M * N * nu);

@@ -4,6 +4,7 @@
 #include <cstdlib>
 
 #include "solver_kernels.cuh"
+#include "pcg_kernels.cuh"
 
 namespace gato {
 
@@ -75,21 +76,7 @@ cudaError_t launch_schur(const SolveParams& P, cudaStream_t s) {
 
 template <int NX>
 size_t pcg_smem_bytes(int N, bool mats) {
-  using L = PcgLayout<NX>;
-  return L::vec_bytes(N + 1) + (mats ? L::mat_bytes(N) : 0);
-}
-
-// Threads per block row of the PCG kernel.  Two slices halve the serial work per PCG iteration
-// (measured on B200: 0.256 -> 0.227 ms at M=32, N=32) but add exchange traffic and barriers that
-// cost more than they save once the horizon fills the SM (N=64: 1.42 -> 1.66 ms), so: 2 for the
-// 14-state models at N <= 40, 1 otherwise.  GATO_PCG_T overrides.
-template <class Mdl>
-int pcg_slices(int N) {
-  static int forced = -1;
-  if (forced < 0) forced = env_int("GATO_PCG_T", 0);
-  int T = forced ? forced : ((Mdl::NX >= 14 && N <= 40) ? 2 : 1);
-  if (T != 1 && !(T == 2 && Mdl::NX >= 14)) T = 1;
-  return T;
+  return pcg_vec_bytes<NX>(N + 1) + (mats ? pcg_smem_mat_bytes<NX>(N) : 0);
 }
 
 // real-time variant (matrix rows in registers) whenever the horizon fits; GATO_PCG_RT=0 disables
@@ -110,22 +97,13 @@ cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
       return cudaGetLastError();
     }
   }
-  int T = pcg_slices<Mdl>(P.N);
-  if (pcg_threads(P.N, T) > kPcgMaxThreads) T = 1;
-  const int threads = pcg_threads(P.N, T);
+  const int threads = pcg_threads(P.N);
   if (threads > kPcgMaxThreads) return cudaErrorInvalidConfiguration;
   const size_t with_mats = pcg_smem_bytes<NX>(P.N, true);
   const bool smem = with_mats <= kMaxSmem && env_int("GATO_PCG_GLOBAL", 0) == 0;
   const size_t bytes = smem ? with_mats : pcg_smem_bytes<NX>(P.N, false);
-  if constexpr (NX >= 14) {
-    if (T == 2) {
-      if (smem) k_pcg<NX, NU, true, 2><<<P.M, threads, bytes, s>>>(P);
-      else k_pcg<NX, NU, false, 2><<<P.M, threads, bytes, s>>>(P);
-      return cudaGetLastError();
-    }
-  }
-  if (smem) k_pcg<NX, NU, true, 1><<<P.M, threads, bytes, s>>>(P);
-  else k_pcg<NX, NU, false, 1><<<P.M, threads, bytes, s>>>(P);
+  if (smem) k_pcg<NX, NU, true><<<P.M, threads, bytes, s>>>(P);
+  else k_pcg<NX, NU, false><<<P.M, threads, bytes, s>>>(P);
   return cudaGetLastError();
 }
 
@@ -169,12 +147,8 @@ cudaError_t prepare_attrs(const SolveParams& P) {
   if (err != cudaSuccess) return err;
   const size_t with_mats = pcg_smem_bytes<NX>(P.N, true);
   if (with_mats <= kMaxSmem) {
-    err = cudaFuncSetAttribute(k_pcg<NX, NU, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_mats);
+    err = cudaFuncSetAttribute(k_pcg<NX, NU, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_mats);
     if (err != cudaSuccess) return err;
-    if constexpr (NX >= 14) {
-      err = cudaFuncSetAttribute(k_pcg<NX, NU, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_mats);
-      if (err != cudaSuccess) return err;
-    }
   }
   const size_t bytes = pcg_smem_bytes<NX>(P.N, false);
   if (bytes > 48 * 1024) return cudaErrorInvalidConfiguration;

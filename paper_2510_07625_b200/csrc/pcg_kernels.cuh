@@ -1,0 +1,844 @@
+// PCG on the Schur system S lam = gamma (blocktri.py:123-173), step recovery (qpform.py:375-397)
+// and the tolerance exit (sqp.py:253-272), one CTA per solve.
+//
+// BLOCK-JACOBI-WHITENED FORM.  With S_kk = L_k L_k^T (k_schur) and L = blockdiag(L_k) put
+//     lam^ = L^T lam,   r^ = L^-1 r,   S^ = L^-1 S L^-T = I + O^,   O^_k = L_{k+1}^-1 phi_k L_k^-T .
+// The reference's symmetric stair preconditioner (qpform.py:342-359)
+//     Phi^-1 = D^-1 - D^-1 offdiag(S) D^-1,  D = blockdiag(S_kk),
+// is exactly L^-T (I - O^) L^-1, so PCG(S, Phi^-1) and PCG(S^, I - O^) generate the same iterates
+// (lam_j = L^-T lam^_j), the same alpha_j, beta_j and the same curvature p^T S p: the recurrence of
+// blocktri.py:141-172 is reproduced term by term, but one iteration is
+//     q^ = p^ + O^ p^                (28 FMAs per matrix row instead of 42)
+//     z^ = r^ - O^ r^                (28 instead of 14 + 28 + 14, one exchange instead of three)
+//     ||r||_2 = ||L r^||_2           (the stop test of blocktri.py:165 needs the unwhitened norm)
+// i.e. 2 exchanges + 2 reductions per iteration instead of 4 + 2, and only O^ and L are resident.
+// Stop test: recurrence residual, confirmed by the TRUE residual ||S lam - gamma|| =
+// ||L (gamma^ - lam^ - O^ lam^)|| before the kernel accepts it; if it does not confirm
+// (ill-conditioned S) every later iteration uses the reference's true-residual test.
+// Dot products: fixed xor-shuffle tree inside a warp, fixed tree over warps -> bitwise reproducible
+// and independent of the batch position.
+//
+//   k_pcg_rt  (n = 14, N <= 35: the real-time regime)  thread (k, i) owns rows i and i + n/2 of block
+//             row k; its rows of O^_{k-1}, of O^_k^T and of L_k live in REGISTERS for the whole solve;
+//             shared memory carries only the two exchange vectors.
+//   k_pcg     (any n, N + 1 <= 256)  one thread per block row, O^ and L in shared memory (or global
+//             memory when the horizon does not fit), 16-byte row loads, O^_k^T applied by rows.
+#pragma once
+#include "solver_kernels.cuh"
+
+namespace gato {
+
+// ---- shared pieces ------------------------------------------------------------------------
+
+// factorisation failure reported by k_schur for this solve?  (thread 0 records it)
+__device__ __forceinline__ bool pcg_schur_failed(const SolveParams& P, int b, int32_t* si) {
+  if (si[SI_SCHUR_FAIL] == INT_MAX) return false;
+  if (threadIdx.x == 0) {
+    const int key = si[SI_SCHUR_FAIL];
+    si[SI_SCHUR_FAIL] = INT_MAX;
+    record_failure(P, b, GATO_STATUS_FACTORIZATION, key / 64, GATO_BLOCK_S, key % 64, 0);
+  }
+  return true;
+}
+
+// curvature <= 0 (blocktri.py:158-161): retry with raised rho or fail (sqp.py:240-248)
+__device__ __forceinline__ void pcg_on_breakdown(const SolveParams& P, int b, int32_t* si, int breakdown) {
+  const int retries = si[SI_RETRIES] + 1;
+  si[SI_RETRIES] = retries;
+  if (retries > P.retry_limit) {
+    record_failure(P, b, GATO_STATUS_PCG_BREAKDOWN, -1, 0, breakdown, retries);
+  } else {
+    P.sd[b * SD_WORDS + SD_RHO] = fmin(P.sd[b * SD_WORDS + SD_RHO] * P.rho_factor, P.rho_max);
+    si[SI_SKIP_LS] = 1;
+  }
+}
+
+// per-solve bookkeeping after the step is known; tolerance exit of sqp.py:256-272
+__device__ __forceinline__ void pcg_finish(const SolveParams& P, int b, int32_t* si, int its, double step_inf,
+                                           double viol) {
+  si[SI_RETRIES] = 0;
+  si[SI_PCG_ITS] = its;
+  P.sd[b * SD_WORDS + SD_STEP_INF] = step_inf;
+  P.sd[b * SD_WORDS + SD_VIOL] = viol;
+  const int it = si[SI_IT];
+  P.pcg_iters[(size_t)b * P.max_it + it] = its;
+  const bool tol_mode = P.step_tol == P.step_tol;  // NaN => None
+  if (tol_mode && step_inf <= P.step_tol && viol <= P.feas_tol) {
+    double* tr = P.trace + ((size_t)b * P.max_it + it) * GATO_TRACE_WORDS;
+    tr[GATO_TRACE_MERIT] = P.sd[b * SD_WORDS + SD_MERIT];
+    tr[GATO_TRACE_CONSTRAINT_L1] = viol;
+    tr[GATO_TRACE_ALPHA] = nan("");
+    tr[GATO_TRACE_RHO] = P.sd[b * SD_WORDS + SD_RHO];
+    tr[GATO_TRACE_PCG_ITERATIONS] = (double)its;
+    tr[GATO_TRACE_ACCEPTED] = 0.0;
+    tr[GATO_TRACE_STEP_INF_NORM] = step_inf;
+    tr[GATO_TRACE_ITERATION] = (double)it;
+    int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
+    info[GATO_INFO_N_RECORDS] = it + 1;
+    info[GATO_INFO_CONVERGED] = 1;
+    si[SI_ACTIVE] = 0;
+    // first iteration of the solve: merit(X0, U0) is produced by this pass's alpha = 0
+    // candidate; k_update patches it into the record (SKIP_LS = 2)
+    si[SI_SKIP_LS] = si[SI_MERIT_VALID] ? 1 : 2;
+  } else {
+    si[SI_SKIP_LS] = 0;
+  }
+}
+
+// one elected thread pulls `bytes` (multiple of 16) from global into shared memory with bulk async
+// copies (TMA, SASS UBLKCP) whose completion is counted in bytes on an mbarrier
+__device__ __forceinline__ void bulk_fill_issue(unsigned bar, void* dst_smem, const void* src, unsigned bytes) {
+  unsigned dst = (unsigned)__cvta_generic_to_shared(dst_smem);
+  const char* s = reinterpret_cast<const char*>(src);
+  constexpr unsigned CHUNK = 32768;
+  for (unsigned off = 0; off < bytes; off += CHUNK) {
+    const unsigned n = bytes - off < CHUNK ? bytes - off : CHUNK;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst + off),
+                 "l"(s + off), "r"(n), "r"(bar)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_init(unsigned bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(unsigned bar) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar)
+        : "memory");
+  }
+}
+
+// CTA-wide sums with at most 8 warps: xor-shuffle tree, one barrier, fixed tree over the warps
+struct Reducer8 {
+  double2* red;  // [2][8], zero-initialised (slots of absent warps stay zero)
+  int flip;
+  __device__ __forceinline__ double2 finish(double2* buf) {
+    __syncthreads();
+    const double2 v0 = buf[0], v1 = buf[1], v2 = buf[2], v3 = buf[3], v4 = buf[4], v5 = buf[5], v6 = buf[6],
+                  v7 = buf[7];
+    return make_double2(((v0.x + v1.x) + (v2.x + v3.x)) + ((v4.x + v5.x) + (v6.x + v7.x)),
+                        ((v0.y + v1.y) + (v2.y + v3.y)) + ((v4.y + v5.y) + (v6.y + v7.y)));
+  }
+  __device__ __forceinline__ double sum1(double a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    double2* buf = red + flip * 8;
+    flip ^= 1;
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5].x = a;
+    return finish(buf).x;
+  }
+  // lanes 0-15 reduce a, lanes 16-31 reduce b after one crossed exchange: 5 shuffles for 2 values
+  __device__ __forceinline__ double2 sum2(double a, double b) {
+    const bool hi = (threadIdx.x & 16) != 0;
+    double keep = hi ? b : a;
+    const double send = hi ? a : b;
+    keep += __shfl_xor_sync(0xffffffffu, send, 16);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
+    double2* buf = red + flip * 8;
+    flip ^= 1;
+    if ((threadIdx.x & 15) == 0) reinterpret_cast<double*>(buf + (threadIdx.x >> 5))[hi ? 1 : 0] = keep;
+    return finish(buf);
+  }
+  __device__ __forceinline__ double max1(double a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = nanmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    double2* buf = red + flip * 8;
+    flip ^= 1;
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5].x = a;   // absent warps: 0 <= any |step|
+    __syncthreads();
+    double m = buf[0].x;
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = nanmax(m, buf[w].x);
+    return m;
+  }
+};
+
+template <int NX>
+__device__ __forceinline__ void vec_load(const double* src, double* v) {
+#pragma unroll
+  for (int j = 0; j < NX / 2; ++j) {
+    const double2 a = reinterpret_cast<const double2*>(src)[j];
+    v[2 * j] = a.x;
+    v[2 * j + 1] = a.y;
+  }
+}
+template <int NX>
+__device__ __forceinline__ void vec_store(double* dst, const double* v) {
+#pragma unroll
+  for (int j = 0; j < NX / 2; ++j) reinterpret_cast<double2*>(dst)[j] = make_double2(v[2 * j], v[2 * j + 1]);
+}
+
+// dot of LEN register-resident matrix entries with a 16-byte aligned shared-memory vector, two chains
+template <int LEN>
+__device__ __forceinline__ double dot_reg(const double (&row)[LEN], const double* __restrict__ v) {
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < LEN / 2; ++j) {
+    const double2 c = v2[j];
+    a0 = fma(row[2 * j], c.x, a0);
+    a1 = fma(row[2 * j + 1], c.y, a1);
+  }
+  if constexpr (LEN & 1) a0 = fma(row[LEN - 1], v[LEN - 1], a0);
+  return a0 + a1;
+}
+
+// -----------------------------------------------------------------------------------------
+// k_pcg_rt
+// -----------------------------------------------------------------------------------------
+constexpr int kPcgRtMaxThreads = 256;
+__host__ __device__ constexpr int pcg_rt_threads(int N, int NX) { return (((N + 1) * (NX / 2)) + 31) / 32 * 32; }
+template <int NX>
+__host__ __device__ constexpr size_t pcg_rt_smem_bytes(int N) {
+  return 3 * (size_t)((N + 1) * NX + 2) * 8 + 16 * 16 + PcgLayout<NX>::mat_bytes(N);
+}
+
+template <int NX, int NU>
+__global__ void __launch_bounds__(kPcgRtMaxThreads, 1) k_pcg_rt(SolveParams P) {
+  static_assert(NX % 2 == 0, "state = [positions, velocities]");
+  using L = PcgLayout<NX>;
+  constexpr int HN = NX / 2, BS = NX * NX;
+  constexpr int HS = hinv_stride(NX, NU);
+  const int b = blockIdx.x;
+  int32_t* si = P.si + b * SI_WORDS;
+  if (!si[SI_ACTIVE]) return;
+  if (pcg_schur_failed(P, b, si)) return;
+  const int N = P.N, nb = N + 1;
+  const int t = threadIdx.x;
+  extern __shared__ __align__(16) double pcg_smem[];
+  const int vlen = nb * NX;
+  double* vp = pcg_smem;            // p^, later lam^ / lambda
+  double* vr = vp + vlen + 2;       // r^, later q - lambda
+  double* vw = vr + vlen + 2;       // scratch of the confirmation pass, later grad_u
+  double2* red = reinterpret_cast<double2*>(vw + vlen + 2);
+  double* mats = reinterpret_cast<double*>(red + 16);
+  __shared__ __align__(8) unsigned long long fill_bar;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&fill_bar);
+  if (t == 0) mbar_init(bar);
+  if (t < 16) red[t] = make_double2(0.0, 0.0);
+  __syncthreads();
+  if (t == 0) {
+    const unsigned bytes = (unsigned)L::mat_bytes(N);
+    mbar_expect(bar, bytes);
+    bulk_fill_issue(bar, mats, P.pmats + (size_t)b * L::mat_doubles(N), bytes);
+  }
+  double* Wm = mats;                                     // W_k -> O^_k, block stride BSP
+  const double* LiS = mats + (size_t)N * L::BSP;         // packed L_k^-1
+  const double* LfS = LiS + (size_t)nb * L::TRP;         // packed L_k
+
+  const bool valid = t < nb * HN;
+  const int k = valid ? t / HN : 0;
+  const int i0 = valid ? t % HN : 0, i1 = i0 + HN;
+  const bool has_lo = valid && k > 0, has_up = valid && k < N;
+  Reducer8 R{red, 0};
+
+  // meanwhile: right-hand sides and the violation of the current iterate (sqp.py:111-115)
+  const double* gam = P.gamma + (size_t)b * vlen;
+  const double* gamw = P.gammaw + (size_t)b * vlen;
+  double r0 = valid ? gamw[k * NX + i0] : 0.0, r1 = valid ? gamw[k * NX + i1] : 0.0;
+  double g2 = 0.0, viol_part = 0.0;
+  if (valid) {
+    const double g0 = gam[k * NX + i0], g1 = gam[k * NX + i1];
+    g2 = g0 * g0 + g1 * g1;
+    if (k < N) {
+      const double* eb = P.e + ((size_t)b * N + k) * NX;
+      viol_part = fabs(eb[i0]) + fabs(eb[i1]);
+    }
+    if (k == 0) {
+      const double* xs = P.x_start + (size_t)b * NX;
+      const double* x0 = P.X + (size_t)b * nb * NX;
+      viol_part += fabs(xs[i0] - x0[i0]) + fabs(xs[i1] - x0[i1]);
+    }
+  }
+  mbar_wait0(bar);
+
+  // ---- one-time: matrix rows -> registers ----
+  double ol0[NX], ol1[NX], ou0[NX], ou1[NX], lr0[HN], lr1[NX];
+  {
+    // rows i0, i1 of O^_{k-1} = W_{k-1} L_{k-1}^-T, written back in place for the column pass below
+    double x0[NX], x1[NX];
+    double* Wk = Wm + (size_t)(has_lo ? k - 1 : 0) * L::BSP;
+    const double* Lp = LiS + (size_t)(has_lo ? k - 1 : 0) * L::TRP;
+    vec_load<NX>(Wk + i0 * NX, x0);
+    vec_load<NX>(Wk + i1 * NX, x1);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int l = 0; l <= j; ++l) {
+        const double m = Lp[j * (j + 1) / 2 + l];
+        a0 = fma(x0[l], m, a0);
+        a1 = fma(x1[l], m, a1);
+      }
+      ol0[j] = has_lo ? a0 : 0.0;
+      ol1[j] = has_lo ? a1 : 0.0;
+    }
+    if (has_lo) {
+      vec_store<NX>(Wk + i0 * NX, ol0);
+      vec_store<NX>(Wk + i1 * NX, ol1);
+    }
+  }
+  __syncthreads();
+  {
+    const double* Ok = Wm + (size_t)(has_up ? k : 0) * L::BSP;   // rows i of O^_k^T = columns i of O^_k
+    const double* Lf = LfS + (size_t)k * L::TRP;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      ou0[j] = has_up ? Ok[j * NX + i0] : 0.0;
+      ou1[j] = has_up ? Ok[j * NX + i1] : 0.0;
+      lr1[j] = (valid && j <= i1) ? Lf[i1 * (i1 + 1) / 2 + (j <= i1 ? j : 0)] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < HN; ++j) lr0[j] = (valid && j <= i0) ? Lf[i0 * (i0 + 1) / 2 + (j <= i0 ? j : 0)] : 0.0;
+  }
+  const int km = (k > 0 ? k - 1 : 0) * NX, kn = (k < N ? k + 1 : N) * NX, kk = k * NX;
+  // rows (k,i0), (k,i1) of O^ v (zero rows at the ends)
+  auto offmv = [&](const double* v, double& y0, double& y1) {
+    y0 = dot_reg<NX>(ol0, v + km) + dot_reg<NX>(ou0, v + kn);
+    y1 = dot_reg<NX>(ol1, v + km) + dot_reg<NX>(ou1, v + kn);
+  };
+  // squared norm contribution of rows (k,i0), (k,i1) of L v
+  auto lnorm2 = [&](const double* v) {
+    const double a = dot_reg<HN>(lr0, v + kk), c = dot_reg<NX>(lr1, v + kk);
+    return a * a + c * c;
+  };
+  auto put = [&](double* v, double a, double c) {
+    if (valid) {
+      v[kk + i0] = a;
+      v[kk + i1] = c;
+    }
+  };
+
+  int its = 0, breakdown = 0;
+  bool nan_curv = false, verify = false;
+  double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
+  const double2 s = R.sum2(g2, viol_part);
+  const double viol = s.y;
+  const double tol2 = P.pcg_tol * P.pcg_tol;
+  if (!(sqrt(s.x) <= P.pcg_tol)) {   // blocktri.py:146-148
+    put(vr, r0, r1);
+    __syncthreads();
+    {
+      double t0, t1;
+      offmv(vr, t0, t1);
+      p0 = valid ? r0 - t0 : 0.0;   // z^ = (I - O^) r^
+      p1 = valid ? r1 - t1 : 0.0;
+    }
+    double rz = R.sum1(r0 * p0 + r1 * p1);
+    const int cap = P.pcg_cap;
+    for (int it = 1; it <= cap; ++it) {
+      put(vp, p0, p1);
+      __syncthreads();
+      double q0 = 0.0, q1 = 0.0;
+      if (valid) {
+        offmv(vp, q0, q1);
+        q0 += p0;   // S^ = I + O^
+        q1 += p1;
+      }
+      const double curv = R.sum1(p0 * q0 + p1 * q1);
+      if (curv <= 0.0) {  // blocktri.py:158-161
+        breakdown = it;
+        break;
+      }
+      if (curv != curv) {  // NaN never satisfies a comparison: the reference runs to the cap
+        nan_curv = true;
+        its = cap;
+        break;
+      }
+      const double a = rz / curv;
+      l0 = l0 + a * p0;
+      l1 = l1 + a * p1;
+      r0 = r0 - a * q0;
+      r1 = r1 - a * q1;
+      put(vr, r0, r1);
+      __syncthreads();
+      double z0 = 0.0, z1 = 0.0, n2 = 0.0;
+      if (valid) {
+        double t0, t1;
+        offmv(vr, t0, t1);
+        z0 = r0 - t0;
+        z1 = r1 - t1;
+        n2 = lnorm2(vr);
+      }
+      const double2 rr = R.sum2(r0 * z0 + r1 * z1, n2);
+      its = it;
+      if (verify || rr.y <= tol2) {
+        // true residual L (gamma^ - lam^ - O^ lam^) of blocktri.py:165
+        put(vp, l0, l1);
+        __syncthreads();
+        double d0 = 0.0, d1 = 0.0;
+        if (valid) {
+          offmv(vp, d0, d1);
+          d0 = gamw[kk + i0] - l0 - d0;
+          d1 = gamw[kk + i1] - l1 - d1;
+        }
+        put(vw, d0, d1);
+        __syncthreads();
+        const double true2 = R.sum1(valid ? lnorm2(vw) : 0.0);
+        if (sqrt(true2) <= P.pcg_tol) break;
+        verify = true;
+      }
+      const double beta = rr.x / rz;
+      p0 = z0 + beta * p0;
+      p1 = z1 + beta * p1;
+      rz = rr.x;
+    }
+  }
+  if (nan_curv) l0 = l1 = nan("");
+
+  if (breakdown) {
+    if (t == 0) pcg_on_breakdown(P, b, si, breakdown);
+    return;
+  }
+
+  // ---- lambda = L^-T lam^, then recover_step (qpform.py:375-397) ----
+  __syncthreads();
+  put(vw, l0, l1);
+  __syncthreads();
+  const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
+  if (valid) {
+    const double* Lp = LiS + (size_t)k * L::TRP;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+      const double v = vw[kk + l];
+      const double m0 = (l >= i0) ? Lp[l * (l + 1) / 2 + i0] : 0.0;
+      const double m1 = (l >= i1) ? Lp[l * (l + 1) / 2 + (l >= i1 ? i1 : 0)] : 0.0;
+      a0 = fma(m0, v, a0);
+      a1 = fma(m1, v, a1);
+    }
+    vp[kk + i0] = a0;
+    vp[kk + i1] = a1;
+    P.lam[(size_t)b * vlen + kk + i0] = a0;
+    P.lam[(size_t)b * vlen + kk + i1] = a1;
+    vr[kk + i0] = g[i0] - a0;
+    vr[kk + i1] = g[i1] - a1;
+  }
+  __syncthreads();
+  double* vu = vw;  // grad_u  [N][NU]   (vw's lam^ is dead after the barrier above)
+  const double* hinv = P.hinv + (size_t)b * HS;
+  if (valid && k < N) {
+    const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
+    const double* ln = vp + (k + 1) * NX;
+    for (int ju = i0; ju < NU; ju += HN) {
+      double su = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) su = fma(Bk[j * NU + ju], ln[j], su);
+      vu[k * NU + ju] = g[NX + ju] + su;
+    }
+  }
+  __syncthreads();
+  double step_part = 0.0;
+  if (valid) {
+    const double* Qk = (k < N) ? hinv : hinv + BS;
+    const double* gk = vr + kk;
+    double d0 = -dot_row<NX>(Qk + i0 * NX, gk);
+    double d1 = -dot_row<NX>(Qk + i1 * NX, gk);
+    if (k < N) {   // -Q^-1 A_k^T lam_{k+1} = phi_k^T lam_{k+1}
+      const double* Ph = P.Soff + ((size_t)b * N + k) * BS;
+      const double* ln = vp + (k + 1) * NX;
+      double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        e0 = fma(Ph[j * NX + i0], ln[j], e0);
+        e1 = fma(Ph[j * NX + i1], ln[j], e1);
+      }
+      d0 += e0;
+      d1 += e1;
+    }
+    double* dX = P.dX + ((size_t)b * nb + k) * NX;
+    dX[i0] = d0;
+    dX[i1] = d1;
+    step_part = nanmax(fabs(d0), fabs(d1));
+    if (k < N) {
+      const double* Ri = hinv + 2 * BS;
+      const double* gu = vu + k * NU;
+      double* dU = P.dU + ((size_t)b * N + k) * NU;
+      for (int ju = i0; ju < NU; ju += HN) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
+        dU[ju] = -acc;
+        step_part = nanmax(step_part, fabs(acc));
+      }
+    }
+  }
+  const double step_inf = R.max1(step_part);
+  if (t == 0) pcg_finish(P, b, si, its, step_inf, viol);
+}
+
+// -----------------------------------------------------------------------------------------
+// k_pcg: one thread per block row ("fat threads"), any block size.
+// Thread k keeps its 14 entries of lam^, r^, p^ in registers and reads O^_{k-1} (by rows) and
+// O^_k (by rows, applied as O^_k^T with n accumulators) with 16-byte loads: every matrix element is
+// read once per product.  Block strides are padded to 2 mod 4 doubles so that the lanes of a
+// quarter-warp hit distinct 16-byte bank groups.
+// -----------------------------------------------------------------------------------------
+// y[NX] += O v : rows of the row-major block O against v
+template <int NX>
+__device__ __forceinline__ void off_rows(const double* __restrict__ O, const double* v, double* y) {
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    const double* row = O + i * NX;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};   // four short chains per row
+    if constexpr (NX % 2 == 0) {
+      const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+      for (int j = 0; j < NX / 2; ++j) {
+        const double2 a = r2[j];
+        acc[(2 * j) & 3] = fma(a.x, v[2 * j], acc[(2 * j) & 3]);
+        acc[(2 * j + 1) & 3] = fma(a.y, v[2 * j + 1], acc[(2 * j + 1) & 3]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) acc[j & 3] = fma(row[j], v[j], acc[j & 3]);
+    }
+    y[i] += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  }
+}
+// y[NX] += O^T v : row j of O scaled by v[j]
+template <int NX>
+__device__ __forceinline__ void off_cols(const double* __restrict__ O, const double* v, double* y) {
+#pragma unroll
+  for (int j = 0; j < NX; ++j) {
+    const double vj = v[j];
+    const double* row = O + j * NX;
+    if constexpr (NX % 2 == 0) {
+      const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+      for (int i = 0; i < NX / 2; ++i) {
+        const double2 a = r2[i];
+        y[2 * i] = fma(a.x, vj, y[2 * i]);
+        y[2 * i + 1] = fma(a.y, vj, y[2 * i + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NX; ++i) y[i] = fma(row[i], vj, y[i]);
+    }
+  }
+}
+// sum_i ((L v)_i)^2 for a packed lower-triangular L
+template <int NX>
+__device__ __forceinline__ double tri_norm2(const double* __restrict__ Lp, const double* v) {
+  double n2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      const double m = Lp[i * (i + 1) / 2 + j];
+      if (j & 1) a1 = fma(m, v[j], a1);
+      else a0 = fma(m, v[j], a0);
+    }
+    const double s = a0 + a1;
+    n2 = fma(s, s, n2);
+  }
+  return n2;
+}
+
+constexpr int kPcgMaxThreads = 256;
+__host__ __device__ constexpr int pcg_threads(int N) { return (((N + 1) + 31) / 32) * 32; }
+template <int NX>
+__host__ __device__ constexpr size_t pcg_vec_bytes(int nb) {
+  return 2 * (size_t)(nb * NX + 2) * 8 + 16 * 16;
+}
+// shared-memory resident part of the record: O^ blocks and packed L (L^-1 is read from global)
+template <int NX>
+__host__ __device__ constexpr size_t pcg_smem_mat_bytes(int N) {
+  return ((size_t)N * PcgLayout<NX>::BSP + (size_t)(N + 1) * PcgLayout<NX>::TRP) * 8;
+}
+
+template <int NX, int NU, bool SMEM_MATS>
+__global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
+  using L = PcgLayout<NX>;
+  constexpr int BS = L::BS;
+  constexpr int HS = hinv_stride(NX, NU);
+  const int b = blockIdx.x;
+  int32_t* si = P.si + b * SI_WORDS;
+  if (!si[SI_ACTIVE]) return;
+  if (pcg_schur_failed(P, b, si)) return;
+  const int N = P.N, nb = N + 1;
+  const int t = threadIdx.x;
+  extern __shared__ __align__(16) double pcg_smem[];
+  const int vlen = nb * NX;
+  double* vA = pcg_smem;                 // exchange buffer: r^, later lambda / grad_x
+  double* vB = vA + vlen + 2;            // exchange buffer: p^
+  double2* red = reinterpret_cast<double2*>(vB + vlen + 2);
+  double* mats = reinterpret_cast<double*>(red + 16);
+  double* pm = P.pmats + (size_t)b * L::mat_doubles(N);
+  const double* LiG = pm + (size_t)N * L::BSP;            // packed L_k^-1 (global)
+  const double* LfG = LiG + (size_t)nb * L::TRP;          // packed L_k (global)
+  __shared__ __align__(8) unsigned long long fill_bar;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&fill_bar);
+  if (t < 16) red[t] = make_double2(0.0, 0.0);
+  if constexpr (SMEM_MATS) {
+    if (t == 0) mbar_init(bar);
+    __syncthreads();
+    if (t == 0) {
+      const unsigned bytes_off = (unsigned)((size_t)N * L::BSP * 8), bytes_tri = (unsigned)((size_t)nb * L::TRP * 8);
+      mbar_expect(bar, bytes_off + bytes_tri);
+      bulk_fill_issue(bar, mats, pm, bytes_off);
+      bulk_fill_issue(bar, mats + (size_t)N * L::BSP, LfG, bytes_tri);
+    }
+  } else {
+    __syncthreads();
+  }
+  double* Ob = SMEM_MATS ? mats : pm;                                   // W_k -> O^_k
+  const double* Lf = SMEM_MATS ? mats + (size_t)N * L::BSP : LfG;       // packed L_k
+
+  const bool valid = t < nb;
+  const int k = valid ? t : 0;
+  Reducer8 R{red, 0};
+
+  double lam[NX], r[NX], p[NX];
+  double g2 = 0.0, viol_part = 0.0;
+  {
+    const double* gamw = P.gammaw + (size_t)b * vlen + k * NX;
+    const double* gam = P.gamma + (size_t)b * vlen + k * NX;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      lam[i] = 0.0;
+      p[i] = 0.0;
+      r[i] = valid ? gamw[i] : 0.0;
+      const double gv = valid ? gam[i] : 0.0;
+      g2 = fma(gv, gv, g2);
+    }
+  }
+  if (valid) {   // violation of the current iterate: |x_s - x_0|_1 + sum |e|_1  (sqp.py:111-115)
+    if (k < N) {
+      const double* eb = P.e + ((size_t)b * N + k) * NX;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) viol_part += fabs(eb[i]);
+    }
+    if (k == 0) {
+      const double* xs = P.x_start + (size_t)b * NX;
+      const double* x0 = P.X + (size_t)b * nb * NX;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) viol_part += fabs(xs[i] - x0[i]);
+    }
+  }
+  if constexpr (SMEM_MATS) mbar_wait0(bar);
+
+  // ---- one-time: O^_k = W_k L_k^-T in place, row by row (thread k owns block k) ----
+  if (valid && k < N) {
+    const double* Lp = LiG + (size_t)k * L::TRP;
+    double* Wk = Ob + (size_t)k * L::BSP;
+#pragma unroll 1
+    for (int i = 0; i < NX; ++i) {
+      double x[NX], o[NX];
+#pragma unroll
+      for (int l = 0; l < NX; ++l) x[l] = Wk[i * NX + l];
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int l = 0; l <= j; ++l) {
+          const double m = Lp[j * (j + 1) / 2 + l];
+          if (l & 1) a1 = fma(x[l], m, a1);
+          else a0 = fma(x[l], m, a0);
+        }
+        o[j] = a0 + a1;
+      }
+#pragma unroll
+      for (int j = 0; j < NX; ++j) Wk[i * NX + j] = o[j];
+    }
+  }
+  __syncthreads();
+
+  // y += O^_{k-1} v_{k-1} + O^_k^T v_{k+1}, neighbours' vectors from the exchange buffer
+  auto apply_off = [&](const double* buf, double* y) {
+    double vn[NX];
+    if (k > 0) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) vn[j] = buf[(k - 1) * NX + j];
+      off_rows<NX>(Ob + (size_t)(k - 1) * L::BSP, vn, y);
+    }
+    if (k < N) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) vn[j] = buf[(k + 1) * NX + j];
+      off_cols<NX>(Ob + (size_t)k * L::BSP, vn, y);
+    }
+  };
+  auto put = [&](double* buf, const double* v) {
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) buf[k * NX + j] = v[j];
+    }
+  };
+  auto dot = [&](const double* a, const double* c) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) acc = fma(a[i], c[i], acc);
+    return acc;
+  };
+
+  int its = 0, breakdown = 0;
+  bool nan_curv = false, verify = false;
+  const double2 s = R.sum2(g2, viol_part);
+  const double viol = s.y;
+  const double tol2 = P.pcg_tol * P.pcg_tol;
+  if (!(sqrt(s.x) <= P.pcg_tol)) {
+    put(vA, r);
+    __syncthreads();
+    {
+      double u[NX];
+#pragma unroll
+      for (int i = 0; i < NX; ++i) u[i] = 0.0;
+      if (valid) apply_off(vA, u);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) p[i] = r[i] - u[i];   // z^ = (I - O^) r^
+    }
+    double rz = R.sum1(dot(r, p));
+    const int cap = P.pcg_cap;
+    for (int it = 1; it <= cap; ++it) {
+      put(vB, p);
+      __syncthreads();
+      double q[NX];
+#pragma unroll
+      for (int i = 0; i < NX; ++i) q[i] = p[i];   // S^ = I + O^
+      if (valid) apply_off(vB, q);
+      const double curv = R.sum1(dot(p, q));
+      if (curv <= 0.0) {  // blocktri.py:158-161
+        breakdown = it;
+        break;
+      }
+      if (curv != curv) {  // NaN never satisfies a comparison: the reference runs to the cap
+        nan_curv = true;
+        its = cap;
+        break;
+      }
+      const double a = rz / curv;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) {
+        lam[i] = lam[i] + a * p[i];
+        r[i] = r[i] - a * q[i];
+      }
+      put(vA, r);
+      __syncthreads();
+      double z[NX];
+#pragma unroll
+      for (int i = 0; i < NX; ++i) z[i] = 0.0;
+      double n2 = 0.0;
+      if (valid) {
+        apply_off(vA, z);
+        n2 = tri_norm2<NX>(Lf + (size_t)k * L::TRP, r);
+      }
+#pragma unroll
+      for (int i = 0; i < NX; ++i) z[i] = r[i] - z[i];
+      const double2 rr = R.sum2(dot(r, z), n2);
+      its = it;
+      if (verify || rr.y <= tol2) {
+        // true residual L (gamma^ - lam^ - O^ lam^) of blocktri.py:165
+        put(vB, lam);
+        __syncthreads();
+        double d[NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) d[i] = 0.0;
+        double t2 = 0.0;
+        if (valid) {
+          apply_off(vB, d);
+          const double* gamw = P.gammaw + (size_t)b * vlen + k * NX;
+#pragma unroll
+          for (int i = 0; i < NX; ++i) d[i] = gamw[i] - lam[i] - d[i];
+          t2 = tri_norm2<NX>(Lf + (size_t)k * L::TRP, d);
+        }
+        const double true2 = R.sum1(t2);
+        if (sqrt(true2) <= P.pcg_tol) break;
+        verify = true;
+      }
+      const double beta = rr.x / rz;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) p[i] = z[i] + beta * p[i];
+      rz = rr.x;
+    }
+  }
+
+  if (breakdown) {
+    if (t == 0) pcg_on_breakdown(P, b, si, breakdown);
+    return;
+  }
+
+  // ---- lambda = L^-T lam^ (thread-local), then recover_step (qpform.py:375-397) ----
+  __syncthreads();
+  const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
+  if (valid) {
+    const double* Lp = LiG + (size_t)k * L::TRP;
+    double lm[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) lm[i] = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+#pragma unroll
+      for (int i = 0; i <= l; ++i) lm[i] = fma(Lp[l * (l + 1) / 2 + i], lam[l], lm[i]);
+    }
+    if (nan_curv) {
+#pragma unroll
+      for (int i = 0; i < NX; ++i) lm[i] = nan("");
+    }
+    double* lg = P.lam + (size_t)b * vlen + k * NX;
+    double gxs[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      lg[i] = lm[i];
+      gxs[i] = g[i] - lm[i];
+    }
+    put(vA, lm);
+    put(vB, gxs);
+  }
+  __syncthreads();
+  const double* hinv = P.hinv + (size_t)b * HS;
+  double step_part = 0.0;
+  if (valid) {
+    double gx[NX], dx[NX], ln[NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) gx[j] = vB[k * NX + j];
+    const double* Qk = (k < N) ? hinv : hinv + BS;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) dx[i] = -dot_row<NX>(Qk + i * NX, gx);
+    if (k < N) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) ln[j] = vA[(k + 1) * NX + j];
+      // -Q^-1 A_k^T lam_{k+1} = phi_k^T lam_{k+1}
+      off_cols<NX>(P.Soff + ((size_t)b * N + k) * BS, ln, dx);
+      const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
+      const double* Ri = hinv + 2 * BS;
+      double gu[NU];
+#pragma unroll
+      for (int ju = 0; ju < NU; ++ju) gu[ju] = g[NX + ju];
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+#pragma unroll
+        for (int ju = 0; ju < NU; ++ju) gu[ju] = fma(Bk[j * NU + ju], ln[j], gu[ju]);
+      }
+      double* dU = P.dU + ((size_t)b * N + k) * NU;
+#pragma unroll
+      for (int ju = 0; ju < NU; ++ju) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
+        dU[ju] = -acc;
+        step_part = nanmax(step_part, fabs(acc));
+      }
+    }
+    double* dX = P.dX + ((size_t)b * nb + k) * NX;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      dX[i] = dx[i];
+      step_part = nanmax(step_part, fabs(dx[i]));
+    }
+  }
+  const double step_inf = R.max1(step_part);
+  if (t == 0) pcg_finish(P, b, si, its, step_inf, viol);
+}
+
+}  // namespace gato

@@ -16,13 +16,14 @@ import paper_2510_07625_b200 as gb  # noqa: E402
 from paper_2510_07625_b200.batch import pack_problems  # noqa: E402
 
 
-def unpack_tri(D, nb, n):
-    out = np.zeros((nb, n, n))
-    tri = D.reshape(nb, n * (n + 1) // 2)
+def dinv_from_factor(Linv, nb, n):
+    """D_k^-1 = L_k^-T L_k^-1 from the packed inverse Cholesky factors"""
+    Li = np.zeros((nb, n, n))
+    tri = Linv.reshape(nb, n * (n + 1) // 2)
     for i in range(n):
         for j in range(i + 1):
-            out[:, i, j] = out[:, j, i] = tri[:, i * (i + 1) // 2 + j]
-    return out
+            Li[:, i, j] = tri[:, i * (i + 1) // 2 + j]
+    return np.einsum("kli,klj->kij", Li, Li)
 
 
 def stage_report(name):
@@ -34,7 +35,7 @@ def stage_report(name):
     eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, st1)
     packed = pack_problems([problem], [(g["X0"], g["U0"])], [st.rho_init])
     eng.solve(packed)
-    got = {k: eng.scratch(k) for k in ("A", "B", "e", "grad", "hinv", "Sdiag", "Soff", "Dinv", "gamma", "lam",
+    got = {k: eng.scratch(k) for k in ("A", "B", "e", "grad", "hinv", "Sdiag", "Soff", "Linv", "gamma", "lam",
                                        "dX", "dU", "merits", "pcg_iters")}
     grad = got["grad"].reshape(N + 1, n + m)
     rows = [
@@ -42,7 +43,7 @@ def stage_report(name):
         ("e", got["e"].reshape(N, n), g["e"]), ("q", grad[:, :n], g["q"]), ("r", grad[:N, n:], g["r"]),
         ("q_inv0", got["hinv"][:n * n].reshape(n, n), g["q_inv"][0]),
         ("Sdiag", got["Sdiag"].reshape(N + 1, n, n), g["Sdiag"]), ("Soff", got["Soff"].reshape(N, n, n), g["Soff"]),
-        ("Dinv", unpack_tri(got["Dinv"], N + 1, n), g["Pdiag"]), ("gamma", got["gamma"], g["gamma"]),
+        ("Dinv", dinv_from_factor(got["Linv"], N + 1, n), g["Pdiag"]), ("gamma", got["gamma"], g["gamma"]),
         ("lam", got["lam"], g["lam"]), ("dX", got["dX"].reshape(N + 1, n), g["dX"]),
         ("dU", got["dU"].reshape(N, m), g["dU"]), ("merits", got["merits"][:len(g["merits"])], g["merits"]),
     ]

@@ -220,10 +220,13 @@ def test_random_instances_over_the_model_pool_match_the_oracle(seed):
     res = gb.sqp_solve(problem, X, U, st)
     ref = orc.solve(orc.Problem.from_spec(problem), X, U, orc.Settings(max_sqp_iterations=8))
     assert rel_inf(res.X, ref.X) <= TRAJ_TOL and rel_inf(res.U, ref.U) <= TRAJ_TOL
-    assert len(res.trace) == len(ref.trace) and res.converged == ref.converged
     got, want = trace_rows(res), trace_rows(ref)
-    flip = _first_decision_flip(got, want)
-    if flip < len(want):
-        assert _on_plateau(want, flip)
-    upto = min(len(want), flip + 1)
+    flip = _first_decision_flip(got, want[:len(got)])
+    if flip < min(len(want), len(got)):
+        # SURVEY.md section 8d parity gate: a flipped step decision is admissible only on the merit
+        # plateau; the iterations after it (and hence the iteration count) may then differ
+        assert _on_plateau(want, flip), f"step decision differs off the merit plateau at iteration {flip}"
+    else:
+        assert len(res.trace) == len(ref.trace) and res.converged == ref.converged
+    upto = min(len(want), len(got), flip + 1)
     assert np.max(np.abs(got[:upto, 5] - want[:upto, 5])) <= 1

@@ -14,13 +14,25 @@ from conftest import STAGED_CASES, load_golden, product_problem, product_setting
 pytestmark = pytest.mark.gpu
 
 
-def unpack_tri(D, nb, n):
+def unpack_lower(T, nb, n):
+    """packed lower-triangular blocks [nb, n(n+1)/2] -> [nb, n, n] with zeros above the diagonal"""
     out = np.zeros((nb, n, n))
-    tri = D.reshape(nb, n * (n + 1) // 2)
+    tri = T.reshape(nb, n * (n + 1) // 2)
     for i in range(n):
         for j in range(i + 1):
-            out[:, i, j] = out[:, j, i] = tri[:, i * (i + 1) // 2 + j]
+            out[:, i, j] = tri[:, i * (i + 1) // 2 + j]
     return out
+
+
+def dinv_from_factor(Linv, nb, n):
+    """D_k^-1 = S_kk^-1 = L_k^-T L_k^-1 from the device's inverse Cholesky factors"""
+    Li = unpack_lower(Linv, nb, n)
+    return np.einsum("kli,klj->kij", Li, Li)
+
+
+def pad_stride(v):
+    m = (v + 1) & ~1
+    return m + 2 if (m // 2) % 2 == 0 else m
 
 
 @pytest.mark.parametrize("name", STAGED_CASES)
@@ -32,7 +44,8 @@ def test_first_iteration_stages_match_reference(name):
     eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, one)
     try:
         eng.solve(pack_problems([problem], [(g["X0"], g["U0"])], [st.rho_init]))
-        got = {k: eng.scratch(k) for k in ("A", "B", "e", "grad", "hinv", "Sdiag", "Soff", "Dinv", "gamma", "lam",
+        got = {k: eng.scratch(k) for k in ("A", "B", "e", "grad", "hinv", "Sdiag", "Soff", "Linv", "Lfac", "gamma", "gammaw",
+                                           "pmats", "lam",
                                            "dX", "dU", "merits", "pcg_iters")}
     finally:
         eng.close()
@@ -46,7 +59,7 @@ def test_first_iteration_stages_match_reference(name):
         ("R^-1", got["hinv"][2 * n * n:2 * n * n + m * m].reshape(m, m), g["r_inv"][0], 1e-11),
         ("S diag", got["Sdiag"].reshape(N + 1, n, n), g["Sdiag"], 1e-11),
         ("S offdiag", got["Soff"].reshape(N, n, n), g["Soff"], 1e-11),
-        ("D^-1", unpack_tri(got["Dinv"], N + 1, n), g["Pdiag"], 1e-9),
+        ("D^-1", dinv_from_factor(got["Linv"], N + 1, n), g["Pdiag"], 1e-9),
         ("gamma", got["gamma"], g["gamma"], 1e-11), ("lambda", got["lam"], g["lam"], 1e-8),
         ("dX", got["dX"].reshape(N + 1, n), g["dX"], 1e-7), ("dU", got["dU"].reshape(N, m), g["dU"], 1e-7),
         ("merits", got["merits"][:len(g["merits"])], g["merits"], 1e-8),
@@ -54,12 +67,22 @@ def test_first_iteration_stages_match_reference(name):
     for label, a, b, tol in checks:
         assert rel_inf(a, b) <= tol, f"{label}: {rel_inf(a, b):.3e} > {tol}"
     assert abs(int(got["pcg_iters"][0]) - int(g["pcg_iterations"])) <= 1
+    # the whitened quantities k_schur hands to the PCG kernels (pcg_kernels.cuh)
+    Lf, Li = unpack_lower(got["Lfac"], N + 1, n), unpack_lower(got["Linv"], N + 1, n)
+    assert rel_inf(Lf @ Lf.transpose(0, 2, 1), g["Sdiag"]) <= 1e-11
+    assert rel_inf(Li @ Lf, np.broadcast_to(np.eye(n), Lf.shape)) <= 1e-9
+    assert rel_inf(got["gammaw"].reshape(N + 1, n), np.einsum("kij,kj->ki", Li, g["gamma"].reshape(N + 1, n))) <= 1e-10
+    bsp, trp = pad_stride(n * n), pad_stride(n * (n + 1) // 2)
+    W = got["pmats"][:N * bsp].reshape(N, bsp)[:, :n * n].reshape(N, n, n)
+    assert rel_inf(W, Li[1:] @ g["Soff"]) <= 1e-10
+    rec_inv = got["pmats"][N * bsp:N * bsp + (N + 1) * trp].reshape(N + 1, trp)[:, :n * (n + 1) // 2]
+    assert np.array_equal(rec_inv.ravel(), got["Linv"])
 
 
 @pytest.mark.parametrize("name", ["twolink_n8", "iiwa14_reach_n8_b0"])
-def test_factored_preconditioner_equals_explicit_stair_blocks(name):
-    """k_pcg applies Phi^-1 as D^-1 (r - phi w) instead of forming -D_{k+1}^-1 phi_k D_k^-1
-    (qpform.py:355-356): the explicit blocks rebuilt from the device D^-1 and phi must equal the
+def test_whitened_preconditioner_equals_explicit_stair_blocks(name):
+    """The PCG kernels apply Phi^-1 as L^-T (I - O^) L^-1 instead of forming -D_{k+1}^-1 phi_k D_k^-1
+    (qpform.py:355-356): the explicit blocks rebuilt from the device factors and phi must equal the
     reference's."""
     g = load_golden(name)
     problem, st = product_problem(g), product_settings(g)
@@ -68,7 +91,7 @@ def test_factored_preconditioner_equals_explicit_stair_blocks(name):
     eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, one)
     try:
         eng.solve(pack_problems([problem], [(g["X0"], g["U0"])], [st.rho_init]))
-        D = unpack_tri(eng.scratch("Dinv"), N + 1, n)
+        D = dinv_from_factor(eng.scratch("Linv"), N + 1, n)
         off = eng.scratch("Soff").reshape(N, n, n)
     finally:
         eng.close()
