@@ -484,26 +484,27 @@ __global__ void __launch_bounds__(kPcgRtMaxThreads, 1) k_pcg_rt(SolveParams P) {
 // read once per product.  Block strides are padded to 2 mod 4 doubles so that the lanes of a
 // quarter-warp hit distinct 16-byte bank groups.
 // -----------------------------------------------------------------------------------------
-// y[NX] += O v : rows of the row-major block O against v
+// One pass over the row-major block O = O^_k serving BOTH products that involve it:
+//   u[i]  = (O own)[i]        -> contribution to block row k+1 (handed over through shared memory)
+//   w[j] += (O^T vn)[j]       -> contribution to the thread's own block row k
+// every matrix element is loaded once (16-byte row loads) and used for two FMAs.
 template <int NX>
-__device__ __forceinline__ void off_rows(const double* __restrict__ O, const double* v, double* y) {
+__device__ __forceinline__ void off_both(const double* __restrict__ O, const double* own, const double* vn, double* u,
+                                         double* w) {
 #pragma unroll
   for (int i = 0; i < NX; ++i) {
-    const double* row = O + i * NX;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};   // four short chains per row
-    if constexpr (NX % 2 == 0) {
-      const double2* r2 = reinterpret_cast<const double2*>(row);
+    const double2* r2 = reinterpret_cast<const double2*>(O + i * NX);
+    const double vi = vn[i];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};   // four short chains per row dot
 #pragma unroll
-      for (int j = 0; j < NX / 2; ++j) {
-        const double2 a = r2[j];
-        acc[(2 * j) & 3] = fma(a.x, v[2 * j], acc[(2 * j) & 3]);
-        acc[(2 * j + 1) & 3] = fma(a.y, v[2 * j + 1], acc[(2 * j + 1) & 3]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < NX; ++j) acc[j & 3] = fma(row[j], v[j], acc[j & 3]);
+    for (int j = 0; j < NX / 2; ++j) {
+      const double2 a = r2[j];
+      acc[(2 * j) & 3] = fma(a.x, own[2 * j], acc[(2 * j) & 3]);
+      acc[(2 * j + 1) & 3] = fma(a.y, own[2 * j + 1], acc[(2 * j + 1) & 3]);
+      w[2 * j] = fma(a.x, vi, w[2 * j]);
+      w[2 * j + 1] = fma(a.y, vi, w[2 * j + 1]);
     }
-    y[i] += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    u[i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
 }
 // y[NX] += O^T v : row j of O scaled by v[j]
@@ -571,8 +572,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   const int t = threadIdx.x;
   extern __shared__ __align__(16) double pcg_smem[];
   const int vlen = nb * NX;
-  double* vA = pcg_smem;                 // exchange buffer: r^, later lambda / grad_x
-  double* vB = vA + vlen + 2;            // exchange buffer: p^
+  double* vA = pcg_smem;                 // exchange buffer: p^ / r^, later lambda
+  double* vB = vA + vlen + 2;            // hand-over buffer: u_k = O^_k v_k, later grad_x
   double2* red = reinterpret_cast<double2*>(vB + vlen + 2);
   double* mats = reinterpret_cast<double*>(red + 16);
   double* pm = P.pmats + (size_t)b * L::mat_doubles(N);
@@ -655,31 +656,46 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   }
   __syncthreads();
 
-  // y += O^_{k-1} v_{k-1} + O^_k^T v_{k+1}, neighbours' vectors from the exchange buffer
-  auto apply_off = [&](const double* buf, double* y) {
-    double vn[NX];
-    if (k > 0) {
-#pragma unroll
-      for (int j = 0; j < NX; ++j) vn[j] = buf[(k - 1) * NX + j];
-      off_rows<NX>(Ob + (size_t)(k - 1) * L::BSP, vn, y);
-    }
-    if (k < N) {
-#pragma unroll
-      for (int j = 0; j < NX; ++j) vn[j] = buf[(k + 1) * NX + j];
-      off_cols<NX>(Ob + (size_t)k * L::BSP, vn, y);
-    }
-  };
+  // (O^ v)_k = O^_{k-1} v_{k-1} + O^_k^T v_{k+1}.  Thread k reads its block O^_k ONCE per product and
+  // forms both u_k = O^_k v_k (which belongs to block row k+1, handed over through vB) and
+  // w_k = O^_k^T v_{k+1} (its own).  The dot products the recurrence needs follow from w alone,
+  //   v^T O^ v = 2 sum_k v_k . w_k        (since v_{k+1} . u_k = v_k . w_k),
+  // so the hand-over of u shares the barrier of the reduction: two exchanges + two reductions = four
+  // barriers per PCG iteration.
   auto put = [&](double* buf, const double* v) {
-    if (valid) {
-#pragma unroll
-      for (int j = 0; j < NX; ++j) buf[k * NX + j] = v[j];
-    }
+    if (valid) vec_store<NX>(buf + k * NX, v);
   };
   auto dot = [&](const double* a, const double* c) {
-    double acc = 0.0;
+    double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) acc = fma(a[i], c[i], acc);
-    return acc;
+    for (int i = 0; i < NX; i += 2) {
+      a0 = fma(a[i], c[i], a0);
+      a1 = fma(a[i + 1], c[i + 1], a1);
+    }
+    return a0 + a1;
+  };
+  const bool has_blk = valid && k < N;
+  const double* Ok = Ob + (size_t)(has_blk ? k : 0) * L::BSP;
+  // v (own block, registers) was published in vA before the last barrier; leaves w, publishes u in vB
+  auto half_products = [&](const double* v, double* w) {
+    double u[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) w[i] = u[i] = 0.0;
+    if (has_blk) {
+      double vn[NX];
+      vec_load<NX>(vA + (k + 1) * NX, vn);
+      off_both<NX>(Ok, v, vn, u, w);
+      vec_store<NX>(vB + k * NX, u);
+    }
+  };
+  // after the barrier that follows half_products: w += u_{k-1}
+  auto add_lower = [&](double* w) {
+    if (valid && k > 0) {
+      double ul[NX];
+      vec_load<NX>(vB + (k - 1) * NX, ul);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) w[i] += ul[i];
+    }
   };
 
   int its = 0, breakdown = 0;
@@ -687,27 +703,22 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   const double2 s = R.sum2(g2, viol_part);
   const double viol = s.y;
   const double tol2 = P.pcg_tol * P.pcg_tol;
+  const double* Lk = Lf + (size_t)k * L::TRP;
   if (!(sqrt(s.x) <= P.pcg_tol)) {
+    double w[NX];
     put(vA, r);
     __syncthreads();
-    {
-      double u[NX];
+    half_products(r, w);
+    double rz = R.sum1(dot(r, r) - 2.0 * dot(r, w));   // r^ . (I - O^) r^
+    add_lower(w);
 #pragma unroll
-      for (int i = 0; i < NX; ++i) u[i] = 0.0;
-      if (valid) apply_off(vA, u);
-#pragma unroll
-      for (int i = 0; i < NX; ++i) p[i] = r[i] - u[i];   // z^ = (I - O^) r^
-    }
-    double rz = R.sum1(dot(r, p));
+    for (int i = 0; i < NX; ++i) p[i] = r[i] - w[i];   // z^ = (I - O^) r^
     const int cap = P.pcg_cap;
     for (int it = 1; it <= cap; ++it) {
-      put(vB, p);
+      put(vA, p);
       __syncthreads();
-      double q[NX];
-#pragma unroll
-      for (int i = 0; i < NX; ++i) q[i] = p[i];   // S^ = I + O^
-      if (valid) apply_off(vB, q);
-      const double curv = R.sum1(dot(p, q));
+      half_products(p, w);
+      const double curv = R.sum1(dot(p, p) + 2.0 * dot(p, w));   // p^ . (I + O^) p^
       if (curv <= 0.0) {  // blocktri.py:158-161
         breakdown = it;
         break;
@@ -717,40 +728,35 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
         its = cap;
         break;
       }
+      add_lower(w);
       const double a = rz / curv;
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
         lam[i] = lam[i] + a * p[i];
-        r[i] = r[i] - a * q[i];
+        r[i] = r[i] - a * (p[i] + w[i]);   // q^ = (I + O^) p^
       }
       put(vA, r);
       __syncthreads();
-      double z[NX];
-#pragma unroll
-      for (int i = 0; i < NX; ++i) z[i] = 0.0;
-      double n2 = 0.0;
-      if (valid) {
-        apply_off(vA, z);
-        n2 = tri_norm2<NX>(Lf + (size_t)k * L::TRP, r);
-      }
-#pragma unroll
-      for (int i = 0; i < NX; ++i) z[i] = r[i] - z[i];
-      const double2 rr = R.sum2(dot(r, z), n2);
+      half_products(r, w);
+      const double n2 = valid ? tri_norm2<NX>(Lk, r) : 0.0;
+      const double2 rr = R.sum2(dot(r, r) - 2.0 * dot(r, w), n2);
+      add_lower(w);
       its = it;
       if (verify || rr.y <= tol2) {
         // true residual L (gamma^ - lam^ - O^ lam^) of blocktri.py:165
-        put(vB, lam);
-        __syncthreads();
         double d[NX];
-#pragma unroll
-        for (int i = 0; i < NX; ++i) d[i] = 0.0;
+        __syncthreads();   // every u of this iteration has been consumed
+        put(vA, lam);
+        __syncthreads();
+        half_products(lam, d);
+        __syncthreads();
+        add_lower(d);
         double t2 = 0.0;
         if (valid) {
-          apply_off(vB, d);
           const double* gamw = P.gammaw + (size_t)b * vlen + k * NX;
 #pragma unroll
           for (int i = 0; i < NX; ++i) d[i] = gamw[i] - lam[i] - d[i];
-          t2 = tri_norm2<NX>(Lf + (size_t)k * L::TRP, d);
+          t2 = tri_norm2<NX>(Lk, d);
         }
         const double true2 = R.sum1(t2);
         if (sqrt(true2) <= P.pcg_tol) break;
@@ -758,7 +764,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
       }
       const double beta = rr.x / rz;
 #pragma unroll
-      for (int i = 0; i < NX; ++i) p[i] = z[i] + beta * p[i];
+      for (int i = 0; i < NX; ++i) p[i] = (r[i] - w[i]) + beta * p[i];   // z^ + beta p^
       rz = rr.x;
     }
   }
