@@ -219,7 +219,7 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
     set_error(h, "batch, horizon, max_sqp_iterations must be >= 1 and timestep > 0");
     return GATO_E_INVALID;
   }
-  if (cfg->horizon + 1 > kPcgMaxThreads) {
+  if (cfg->horizon + 1 > 256) {
     set_error(h, "horizon too long: the PCG kernel runs one thread per block row, N + 1 <= 256");
     return GATO_E_INVALID;
   }
@@ -258,6 +258,7 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   ALLOC(pmats, M * (int64_t)h->ops.pcg_mat_doubles((int)N));
   ALLOC(gamma, M * nb * nx);
   ALLOC(gammaw, M * nb * nx);
+  ALLOC(lbw, M * nb);
   ALLOC(lam, M * nb * nx);
   ALLOC(dX, M * nb * nx);
   ALLOC(dU, M * N * nu);

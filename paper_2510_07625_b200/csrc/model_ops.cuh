@@ -74,11 +74,6 @@ cudaError_t launch_schur(const SolveParams& P, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int NX>
-size_t pcg_smem_bytes(int N, bool mats) {
-  return pcg_vec_bytes<NX>(N + 1) + (mats ? pcg_smem_mat_bytes<NX>(N) : 0);
-}
-
 // real-time variant (matrix rows in registers) whenever the horizon fits; GATO_PCG_RT=0 disables
 template <class Mdl>
 bool pcg_use_rt(int N) {
@@ -86,6 +81,53 @@ bool pcg_use_rt(int N) {
   if (allowed < 0) allowed = env_int("GATO_PCG_RT", 1);
   return allowed && Mdl::NX >= 14 && pcg_rt_threads(N, Mdl::NX) <= kPcgRtMaxThreads &&
          pcg_rt_smem_bytes<Mdl::NX>(N) <= kMaxSmem;
+}
+
+// Shapes of the fat-thread PCG kernel: O^ blocks in shared memory when they fit, with the packed L_k
+// resident beside them (one CTA per SM); GATO_PCG_MINB=2 selects the two-CTAs-per-SM build instead
+// (shared memory <= 113 KB, <= 128 threads, L_k read from L2 in the few exact-norm iterations).
+constexpr size_t kHalfSmem = 113 * 1024;
+struct PcgShape {
+  int threads, minb;
+  bool smem, lres;
+  size_t bytes;
+};
+template <class Mdl>
+PcgShape pcg_shape(int N, int M) {
+  constexpr int NX = Mdl::NX;
+  static int forced_minb = -1, sms = 0;
+  if (forced_minb < 0) forced_minb = env_int("GATO_PCG_MINB", 0);
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  PcgShape sh;
+  sh.threads = pcg_threads(N);
+  const size_t with_mats = pcg_smem_bytes<NX>(N, true);
+  sh.smem = with_mats <= kMaxSmem && env_int("GATO_PCG_GLOBAL", 0) == 0;
+  sh.lres = false;
+  sh.bytes = sh.smem ? with_mats : pcg_smem_bytes<NX>(N, false);
+  const bool fits2 = sh.smem && sh.bytes <= kHalfSmem && sh.threads <= 128;
+  // measured on B200 (M = 128 and M = 1024, N = 64): the resident-L build is as fast or faster at both
+  // sizes, so the two-CTA build is opt-in
+  sh.minb = (fits2 && forced_minb == 2) ? 2 : 1;
+  (void)M;
+  if (sh.minb == 1 && sh.smem && pcg_smem_bytes<NX>(N, true, true) <= kMaxSmem) {
+    sh.lres = true;
+    sh.bytes = pcg_smem_bytes<NX>(N, true, true);
+  }
+  return sh;
+}
+
+template <class Mdl, class F>
+cudaError_t pcg_dispatch(const PcgShape& sh, F&& f) {
+  constexpr int NX = Mdl::NX, NU = Mdl::NU;
+  if (sh.threads > 256) return cudaErrorInvalidConfiguration;
+  if (!sh.smem) return f(k_pcg<NX, NU, false, false, 256, 1>);
+  if (sh.minb == 2) return f(k_pcg<NX, NU, true, false, 128, 2>);
+  if (sh.lres) return f(k_pcg<NX, NU, true, true, 256, 1>);
+  return f(k_pcg<NX, NU, true, false, 256, 1>);
 }
 
 template <class Mdl>
@@ -97,14 +139,11 @@ cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
       return cudaGetLastError();
     }
   }
-  const int threads = pcg_threads(P.N);
-  if (threads > kPcgMaxThreads) return cudaErrorInvalidConfiguration;
-  const size_t with_mats = pcg_smem_bytes<NX>(P.N, true);
-  const bool smem = with_mats <= kMaxSmem && env_int("GATO_PCG_GLOBAL", 0) == 0;
-  const size_t bytes = smem ? with_mats : pcg_smem_bytes<NX>(P.N, false);
-  if (smem) k_pcg<NX, NU, true><<<P.M, threads, bytes, s>>>(P);
-  else k_pcg<NX, NU, false><<<P.M, threads, bytes, s>>>(P);
-  return cudaGetLastError();
+  const PcgShape sh = pcg_shape<Mdl>(P.N, P.M);
+  return pcg_dispatch<Mdl>(sh, [&](auto kernel) {
+    kernel<<<P.M, sh.threads, sh.bytes, s>>>(P);
+    return cudaGetLastError();
+  });
 }
 
 template <class Mdl>
@@ -145,13 +184,17 @@ cudaError_t prepare_attrs(const SolveParams& P) {
   err = cudaFuncSetAttribute(k_schur<NX, NU, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(4 * sizeof(SchurSmem<NX, NU>)));
   if (err != cudaSuccess) return err;
-  const size_t with_mats = pcg_smem_bytes<NX>(P.N, true);
-  if (with_mats <= kMaxSmem) {
-    err = cudaFuncSetAttribute(k_pcg<NX, NU, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_mats);
+  {
+    const PcgShape sh = pcg_shape<Mdl>(P.N, P.M);
+    if (!sh.smem && sh.bytes > 48 * 1024) return cudaErrorInvalidConfiguration;
+    err = pcg_dispatch<Mdl>(sh, [&](auto kernel) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.bytes);
+      if (e == cudaSuccess && sh.minb == 2)
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+      return e;
+    });
     if (err != cudaSuccess) return err;
   }
-  const size_t bytes = pcg_smem_bytes<NX>(P.N, false);
-  if (bytes > 48 * 1024) return cudaErrorInvalidConfiguration;
   if constexpr (NX >= 14) {
     if (pcg_rt_smem_bytes<NX>(P.N) <= kMaxSmem) {
       err = cudaFuncSetAttribute(k_pcg_rt<NX, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -478,23 +478,37 @@ __global__ void __launch_bounds__(kPcgRtMaxThreads, 1) k_pcg_rt(SolveParams P) {
 }
 
 // -----------------------------------------------------------------------------------------
-// k_pcg: one thread per block row ("fat threads"), any block size.
-// Thread k keeps its 14 entries of lam^, r^, p^ in registers and reads O^_{k-1} (by rows) and
-// O^_k (by rows, applied as O^_k^T with n accumulators) with 16-byte loads: every matrix element is
-// read once per product.  Block strides are padded to 2 mod 4 doubles so that the lanes of a
-// quarter-warp hit distinct 16-byte bank groups.
+// k_pcg: one thread per block row ("fat threads"), any block size, N + 1 <= 256.
+//
+// Thread k keeps its entries of lam^, r^, p^ in registers and owns the block O^_k.  ONE pass over the
+// block per product serves both of its uses (16-byte row loads, every element loaded once, two FMAs
+// each):
+//     u_k = O^_k v_k          -> belongs to block row k+1
+//     w_k = O^_k^T v_{k+1}    -> belongs to block row k
+// and the dot products of the recurrence follow from w alone,
+//     v^T O^ v = 2 sum_k v_k . w_k           (v_{k+1} . u_k = v_k . w_k),
+// so handing u to the next block row shares the barrier of the reduction.  v_{k+1} and u_{k-1} travel
+// through ONE shared-memory exchange vector (warp shuffles measured ~3x dearer than 16-byte shared
+// loads for this); shared memory holds the O^ blocks plus that vector (N = 64, n = 14: 109 KB -> two
+// CTAs per SM).  KPW block rows per warp: with 16 (lanes
+// 0-15 active) a 65-row solve spreads over four warps, one per SM sub-partition, instead of loading two
+// sub-partitions with full warps and leaving two idle (measured: co-resident CTAs otherwise collide
+// on the same schedulers); half-empty warps cost half the shared-memory wavefronts, so nothing is lost.
+// Stop test: ||r|| = ||L r^|| needs L_k, which is NOT resident.  While the lower bound
+//     ||L r^||^2 >= sum_k ||r^_k||^2 / ||L_k^-1||_F^2     (lbw, from k_schur)
+// exceeds tol^2 the solve cannot have converged; once it does not, the kernel evaluates the exact
+// norm for the remaining iterations -- typically the last 8 of ~57 (measured on the N = 64
+// workloads) -- from the packed L_k in global memory (L2) in the two-CTAs-per-SM build, or from a
+// resident copy (LRES) in the build used when the batch does not fill the SMs twice.
 // -----------------------------------------------------------------------------------------
-// One pass over the row-major block O = O^_k serving BOTH products that involve it:
-//   u[i]  = (O own)[i]        -> contribution to block row k+1 (handed over through shared memory)
-//   w[j] += (O^T vn)[j]       -> contribution to the thread's own block row k
-// every matrix element is loaded once (16-byte row loads) and used for two FMAs.
-template <int NX>
-__device__ __forceinline__ void off_both(const double* __restrict__ O, const double* own, const double* vn, double* u,
-                                         double* w) {
+// u[il] = (O own)[row0 + il],  w[j] += sum_il O[row0 + il][j] vn[il]   for RP rows starting at row0
+template <int NX, int RP>
+__device__ __forceinline__ void off_both(const double* __restrict__ Orows, const double* own, const double* vn,
+                                         double* u, double* w) {
 #pragma unroll
-  for (int i = 0; i < NX; ++i) {
-    const double2* r2 = reinterpret_cast<const double2*>(O + i * NX);
-    const double vi = vn[i];
+  for (int il = 0; il < RP; ++il) {
+    const double2* r2 = reinterpret_cast<const double2*>(Orows + il * NX);
+    const double vi = vn[il];
     double acc[4] = {0.0, 0.0, 0.0, 0.0};   // four short chains per row dot
 #pragma unroll
     for (int j = 0; j < NX / 2; ++j) {
@@ -504,28 +518,18 @@ __device__ __forceinline__ void off_both(const double* __restrict__ O, const dou
       w[2 * j] = fma(a.x, vi, w[2 * j]);
       w[2 * j + 1] = fma(a.y, vi, w[2 * j + 1]);
     }
-    u[i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    u[il] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
 }
-// y[NX] += O^T v : row j of O scaled by v[j]
-template <int NX>
-__device__ __forceinline__ void off_cols(const double* __restrict__ O, const double* v, double* y) {
+// y[RP] += (O^T v)[col0 .. col0 + RP): row j of O scaled by v[j]
+template <int NX, int RP>
+__device__ __forceinline__ void off_cols(const double* __restrict__ O, int col0, const double* v, double* y) {
 #pragma unroll
   for (int j = 0; j < NX; ++j) {
     const double vj = v[j];
-    const double* row = O + j * NX;
-    if constexpr (NX % 2 == 0) {
-      const double2* r2 = reinterpret_cast<const double2*>(row);
+    const double* seg = O + j * NX + col0;
 #pragma unroll
-      for (int i = 0; i < NX / 2; ++i) {
-        const double2 a = r2[i];
-        y[2 * i] = fma(a.x, vj, y[2 * i]);
-        y[2 * i + 1] = fma(a.y, vj, y[2 * i + 1]);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < NX; ++i) y[i] = fma(row[i], vj, y[i]);
-    }
+    for (int i = 0; i < RP; ++i) y[i] = fma(seg[i], vj, y[i]);
   }
 }
 // sum_i ((L v)_i)^2 for a packed lower-triangular L
@@ -534,48 +538,50 @@ __device__ __forceinline__ double tri_norm2(const double* __restrict__ Lp, const
   double n2 = 0.0;
 #pragma unroll
   for (int i = 0; i < NX; ++i) {
-    double a0 = 0.0, a1 = 0.0;
+    {
+      double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-    for (int j = 0; j <= i; ++j) {
-      const double m = Lp[i * (i + 1) / 2 + j];
-      if (j & 1) a1 = fma(m, v[j], a1);
-      else a0 = fma(m, v[j], a0);
+      for (int j = 0; j <= i; ++j) {
+        const double m = Lp[i * (i + 1) / 2 + j];
+        if (j & 1) a1 = fma(m, v[j], a1);
+        else a0 = fma(m, v[j], a0);
+      }
+      const double s = a0 + a1;
+      n2 = fma(s, s, n2);
     }
-    const double s = a0 + a1;
-    n2 = fma(s, s, n2);
   }
   return n2;
 }
 
-constexpr int kPcgMaxThreads = 256;
-__host__ __device__ constexpr int pcg_threads(int N) { return (((N + 1) + 31) / 32) * 32; }
+__host__ __device__ constexpr int pcg_threads(int N) { return ((N + 1) + 31) / 32 * 32; }
+// shared memory: reduction slots, the exchange vector, then the O^ blocks (or, when they stay in global
+// memory, the two vectors of the step recovery)
 template <int NX>
-__host__ __device__ constexpr size_t pcg_vec_bytes(int nb) {
-  return 2 * (size_t)(nb * NX + 2) * 8 + 16 * 16;
-}
-// shared-memory resident part of the record: O^ blocks and packed L (L^-1 is read from global)
-template <int NX>
-__host__ __device__ constexpr size_t pcg_smem_mat_bytes(int N) {
-  return ((size_t)N * PcgLayout<NX>::BSP + (size_t)(N + 1) * PcgLayout<NX>::TRP) * 8;
+__host__ __device__ constexpr size_t pcg_smem_bytes(int N, bool mats, bool lres = false) {
+  const size_t fixed = 16 * 16 + (size_t)((N + 1) * NX + 2) * 8;
+  const size_t vecs = 2 * (size_t)((N + 1) * NX + 2) * 8;
+  const size_t blocks = (size_t)N * PcgLayout<NX>::BSP * 8 + (lres ? (size_t)(N + 1) * PcgLayout<NX>::TRP * 8 : 0);
+  return fixed + (mats ? (blocks > vecs ? blocks : vecs) : vecs);
 }
 
-template <int NX, int NU, bool SMEM_MATS>
-__global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
+template <int NX, int NU, bool SMEM_MATS, bool LRES, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_pcg(SolveParams P) {
+  constexpr int KPW = 32;
+  static_assert(NX % 2 == 0 && (SMEM_MATS || !LRES), "state = [positions, velocities]; L resident only beside O^");
   using L = PcgLayout<NX>;
-  constexpr int BS = L::BS;
+  constexpr int BS = L::BS, RP = NX;
   constexpr int HS = hinv_stride(NX, NU);
   const int b = blockIdx.x;
   int32_t* si = P.si + b * SI_WORDS;
   if (!si[SI_ACTIVE]) return;
   if (pcg_schur_failed(P, b, si)) return;
   const int N = P.N, nb = N + 1;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   extern __shared__ __align__(16) double pcg_smem[];
   const int vlen = nb * NX;
-  double* vA = pcg_smem;                 // exchange buffer: p^ / r^, later lambda
-  double* vB = vA + vlen + 2;            // hand-over buffer: u_k = O^_k v_k, later grad_x
-  double2* red = reinterpret_cast<double2*>(vB + vlen + 2);
-  double* mats = reinterpret_cast<double*>(red + 16);
+  double2* red = reinterpret_cast<double2*>(pcg_smem);
+  double* xv = reinterpret_cast<double*>(red + 16);     // exchange vector, nb slots of NX
+  double* mats = xv + vlen + 2;
   double* pm = P.pmats + (size_t)b * L::mat_doubles(N);
   const double* LiG = pm + (size_t)N * L::BSP;            // packed L_k^-1 (global)
   const double* LfG = LiG + (size_t)nb * L::TRP;          // packed L_k (global)
@@ -584,21 +590,25 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   if (t < 16) red[t] = make_double2(0.0, 0.0);
   if constexpr (SMEM_MATS) {
     if (t == 0) mbar_init(bar);
-    __syncthreads();
+  }
+  __syncthreads();
+  if constexpr (SMEM_MATS) {
     if (t == 0) {
-      const unsigned bytes_off = (unsigned)((size_t)N * L::BSP * 8), bytes_tri = (unsigned)((size_t)nb * L::TRP * 8);
+      const unsigned bytes_off = (unsigned)((size_t)N * L::BSP * 8);
+      const unsigned bytes_tri = LRES ? (unsigned)((size_t)nb * L::TRP * 8) : 0u;
       mbar_expect(bar, bytes_off + bytes_tri);
       bulk_fill_issue(bar, mats, pm, bytes_off);
-      bulk_fill_issue(bar, mats + (size_t)N * L::BSP, LfG, bytes_tri);
+      if (LRES) bulk_fill_issue(bar, mats + (size_t)N * L::BSP, LfG, bytes_tri);
     }
-  } else {
-    __syncthreads();
   }
-  double* Ob = SMEM_MATS ? mats : pm;                                   // W_k -> O^_k
-  const double* Lf = SMEM_MATS ? mats + (size_t)N * L::BSP : LfG;       // packed L_k
+  double* Ob = SMEM_MATS ? mats : pm;   // W_k -> O^_k
 
-  const bool valid = t < nb;
-  const int k = valid ? t : 0;
+  const int kk = lane;
+  const int krow = warp * KPW + kk;
+  const bool valid = kk < KPW && krow < nb;
+  const int k = valid ? krow : 0;
+  constexpr int row0 = 0;
+  const bool has_blk = valid && k < N;
   Reducer8 R{red, 0};
 
   double lam[NX], r[NX], p[NX];
@@ -628,17 +638,17 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
       for (int i = 0; i < NX; ++i) viol_part += fabs(xs[i] - x0[i]);
     }
   }
+  const double lbw = valid ? P.lbw[(size_t)b * nb + k] : 0.0;
   if constexpr (SMEM_MATS) mbar_wait0(bar);
 
   // ---- one-time: O^_k = W_k L_k^-T in place, row by row (thread k owns block k) ----
-  if (valid && k < N) {
+  double* Ok = Ob + (size_t)(has_blk ? k : 0) * L::BSP;   // the thread's block O^_k
+  if (has_blk) {
     const double* Lp = LiG + (size_t)k * L::TRP;
-    double* Wk = Ob + (size_t)k * L::BSP;
 #pragma unroll 1
-    for (int i = 0; i < NX; ++i) {
+    for (int il = 0; il < NX; ++il) {
       double x[NX], o[NX];
-#pragma unroll
-      for (int l = 0; l < NX; ++l) x[l] = Wk[i * NX + l];
+      vec_load<NX>(Ok + il * NX, x);
 #pragma unroll
       for (int j = 0; j < NX; ++j) {
         double a0 = 0.0, a1 = 0.0;
@@ -650,21 +660,11 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
         }
         o[j] = a0 + a1;
       }
-#pragma unroll
-      for (int j = 0; j < NX; ++j) Wk[i * NX + j] = o[j];
+      vec_store<NX>(Ok + il * NX, o);
     }
   }
   __syncthreads();
 
-  // (O^ v)_k = O^_{k-1} v_{k-1} + O^_k^T v_{k+1}.  Thread k reads its block O^_k ONCE per product and
-  // forms both u_k = O^_k v_k (which belongs to block row k+1, handed over through vB) and
-  // w_k = O^_k^T v_{k+1} (its own).  The dot products the recurrence needs follow from w alone,
-  //   v^T O^ v = 2 sum_k v_k . w_k        (since v_{k+1} . u_k = v_k . w_k),
-  // so the hand-over of u shares the barrier of the reduction: two exchanges + two reductions = four
-  // barriers per PCG iteration.
-  auto put = [&](double* buf, const double* v) {
-    if (valid) vec_store<NX>(buf + k * NX, v);
-  };
   auto dot = [&](const double* a, const double* c) {
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -674,51 +674,54 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
     }
     return a0 + a1;
   };
-  const bool has_blk = valid && k < N;
-  const double* Ok = Ob + (size_t)(has_blk ? k : 0) * L::BSP;
-  // v (own block, registers) was published in vA before the last barrier; leaves w, publishes u in vB
-  auto half_products = [&](const double* v, double* w) {
-    double u[NX];
+  // Exchange through ONE shared-memory vector xv of nb slots.  Before a barrier thread k puts v_k in
+  // slot k; after it, thread k takes v_{k+1} from slot k+1 into registers and -- being the only
+  // reader of that slot -- reuses it for u_k, which is exactly where thread k+1 looks for u after the
+  // next barrier (the one inside the reduction).
+  auto publish_v = [&](const double* v) {
+    if (valid) vec_store<NX>(xv + k * NX, v);
+  };
+  auto half_products = [&](const double* v, double* w, double* u) {
 #pragma unroll
     for (int i = 0; i < NX; ++i) w[i] = u[i] = 0.0;
     if (has_blk) {
       double vn[NX];
-      vec_load<NX>(vA + (k + 1) * NX, vn);
-      off_both<NX>(Ok, v, vn, u, w);
-      vec_store<NX>(vB + k * NX, u);
+      vec_load<NX>(xv + (k + 1) * NX, vn);
+      off_both<NX, NX>(Ok, v, vn, u, w);
+      vec_store<NX>(xv + (k + 1) * NX, u);
     }
   };
   // after the barrier that follows half_products: w += u_{k-1}
-  auto add_lower = [&](double* w) {
+  auto add_lower = [&](const double*, double* w) {
     if (valid && k > 0) {
       double ul[NX];
-      vec_load<NX>(vB + (k - 1) * NX, ul);
+      vec_load<NX>(xv + k * NX, ul);
 #pragma unroll
       for (int i = 0; i < NX; ++i) w[i] += ul[i];
     }
   };
 
   int its = 0, breakdown = 0;
-  bool nan_curv = false, verify = false;
+  bool nan_curv = false, verify = false, exact = false;
   const double2 s = R.sum2(g2, viol_part);
   const double viol = s.y;
   const double tol2 = P.pcg_tol * P.pcg_tol;
-  const double* Lk = Lf + (size_t)k * L::TRP;
+  const double* Lk = (LRES ? mats + (size_t)N * L::BSP : LfG) + (size_t)k * L::TRP;   // packed L_k
   if (!(sqrt(s.x) <= P.pcg_tol)) {
-    double w[NX];
-    put(vA, r);
+    double w[NX], u[RP];
+    publish_v(r);
     __syncthreads();
-    half_products(r, w);
-    double rz = R.sum1(dot(r, r) - 2.0 * dot(r, w));   // r^ . (I - O^) r^
-    add_lower(w);
+    half_products(r, w, u);
+    double rz = R.sum1((dot(r, r) - 2.0 * dot(r, w)));   // r^ . (I - O^) r^
+    add_lower(u, w);
 #pragma unroll
     for (int i = 0; i < NX; ++i) p[i] = r[i] - w[i];   // z^ = (I - O^) r^
     const int cap = P.pcg_cap;
     for (int it = 1; it <= cap; ++it) {
-      put(vA, p);
+      publish_v(p);
       __syncthreads();
-      half_products(p, w);
-      const double curv = R.sum1(dot(p, p) + 2.0 * dot(p, w));   // p^ . (I + O^) p^
+      half_products(p, w, u);
+      const double curv = R.sum1((dot(p, p) + 2.0 * dot(p, w)));   // p^ . (I + O^) p^
       if (curv <= 0.0) {  // blocktri.py:158-161
         breakdown = it;
         break;
@@ -728,29 +731,34 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
         its = cap;
         break;
       }
-      add_lower(w);
+      add_lower(u, w);
       const double a = rz / curv;
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
         lam[i] = lam[i] + a * p[i];
         r[i] = r[i] - a * (p[i] + w[i]);   // q^ = (I + O^) p^
       }
-      put(vA, r);
+      publish_v(r);
       __syncthreads();
-      half_products(r, w);
-      const double n2 = valid ? tri_norm2<NX>(Lk, r) : 0.0;
-      const double2 rr = R.sum2(dot(r, r) - 2.0 * dot(r, w), n2);
-      add_lower(w);
+      half_products(r, w, u);
+      const double rr_own = dot(r, r);
+      double n2 = lbw * rr_own;   // lower bound of this block row's ||L_k r^_k||^2
+      if (exact) n2 = valid ? tri_norm2<NX>(Lk, r) : 0.0;
+      double2 rr = R.sum2(rr_own - 2.0 * dot(r, w), n2);
+      add_lower(u, w);
       its = it;
+      if (!exact && rr.y <= tol2) {   // the bound no longer excludes convergence: exact norm from now on
+        exact = true;
+        rr.y = R.sum1(valid ? tri_norm2<NX>(Lk, r) : 0.0);
+      }
       if (verify || rr.y <= tol2) {
         // true residual L (gamma^ - lam^ - O^ lam^) of blocktri.py:165
-        double d[NX];
-        __syncthreads();   // every u of this iteration has been consumed
-        put(vA, lam);
+        double d[NX], ud[RP];
+        publish_v(lam);
         __syncthreads();
-        half_products(lam, d);
+        half_products(lam, d, ud);
         __syncthreads();
-        add_lower(d);
+        add_lower(ud, d);
         double t2 = 0.0;
         if (valid) {
           const double* gamw = P.gammaw + (size_t)b * vlen + k * NX;
@@ -775,7 +783,9 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
   }
 
   // ---- lambda = L^-T lam^ (thread-local), then recover_step (qpform.py:375-397) ----
-  __syncthreads();
+  __syncthreads();          // the O^ blocks are dead: their shared memory now carries two vectors
+  double* vA = mats;               // lambda
+  double* vB = vA + vlen + 2;      // q - lambda
   const double* g = P.grad + ((size_t)b * nb + k) * (NX + NU);
   if (valid) {
     const double* Lp = LiG + (size_t)k * L::TRP;
@@ -791,56 +801,58 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg(SolveParams P) {
 #pragma unroll
       for (int i = 0; i < NX; ++i) lm[i] = nan("");
     }
-    double* lg = P.lam + (size_t)b * vlen + k * NX;
-    double gxs[NX];
+    {
+      double* lg = P.lam + (size_t)b * vlen + k * NX;
+      double gxs[NX];
 #pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      lg[i] = lm[i];
-      gxs[i] = g[i] - lm[i];
+      for (int i = 0; i < NX; ++i) {
+        lg[i] = lm[i];
+        gxs[i] = g[i] - lm[i];
+      }
+      vec_store<NX>(vA + k * NX, lm);
+      vec_store<NX>(vB + k * NX, gxs);
     }
-    put(vA, lm);
-    put(vB, gxs);
   }
   __syncthreads();
   const double* hinv = P.hinv + (size_t)b * HS;
   double step_part = 0.0;
   if (valid) {
-    double gx[NX], dx[NX], ln[NX];
-#pragma unroll
-    for (int j = 0; j < NX; ++j) gx[j] = vB[k * NX + j];
+    double gx[NX], dx[RP], ln[NX];
+    vec_load<NX>(vB + k * NX, gx);
     const double* Qk = (k < N) ? hinv : hinv + BS;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) dx[i] = -dot_row<NX>(Qk + i * NX, gx);
+    for (int il = 0; il < RP; ++il) dx[il] = -dot_row<NX>(Qk + (row0 + il) * NX, gx);
     if (k < N) {
-#pragma unroll
-      for (int j = 0; j < NX; ++j) ln[j] = vA[(k + 1) * NX + j];
+      vec_load<NX>(vA + (k + 1) * NX, ln);
       // -Q^-1 A_k^T lam_{k+1} = phi_k^T lam_{k+1}
-      off_cols<NX>(P.Soff + ((size_t)b * N + k) * BS, ln, dx);
-      const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
-      const double* Ri = hinv + 2 * BS;
-      double gu[NU];
+      off_cols<NX, RP>(P.Soff + ((size_t)b * N + k) * BS, row0, ln, dx);
+      {   // the control step of this knot
+        const double* Bk = P.B + ((size_t)b * N + k) * NX * NU;
+        const double* Ri = hinv + 2 * BS;
+        double gu[NU];
 #pragma unroll
-      for (int ju = 0; ju < NU; ++ju) gu[ju] = g[NX + ju];
+        for (int ju = 0; ju < NU; ++ju) gu[ju] = g[NX + ju];
 #pragma unroll
-      for (int j = 0; j < NX; ++j) {
+        for (int j = 0; j < NX; ++j) {
 #pragma unroll
-        for (int ju = 0; ju < NU; ++ju) gu[ju] = fma(Bk[j * NU + ju], ln[j], gu[ju]);
-      }
-      double* dU = P.dU + ((size_t)b * N + k) * NU;
+          for (int ju = 0; ju < NU; ++ju) gu[ju] = fma(Bk[j * NU + ju], ln[j], gu[ju]);
+        }
+        double* dU = P.dU + ((size_t)b * N + k) * NU;
 #pragma unroll
-      for (int ju = 0; ju < NU; ++ju) {
-        double acc = 0.0;
+        for (int ju = 0; ju < NU; ++ju) {
+          double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
-        dU[ju] = -acc;
-        step_part = nanmax(step_part, fabs(acc));
+          for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
+          dU[ju] = -acc;
+          step_part = nanmax(step_part, fabs(acc));
+        }
       }
     }
-    double* dX = P.dX + ((size_t)b * nb + k) * NX;
+    double* dX = P.dX + ((size_t)b * nb + k) * NX + row0;
 #pragma unroll
-    for (int i = 0; i < NX; ++i) {
-      dX[i] = dx[i];
-      step_part = nanmax(step_part, fabs(dx[i]));
+    for (int il = 0; il < RP; ++il) {
+      dX[il] = dx[il];
+      step_part = nanmax(step_part, fabs(dx[il]));
     }
   }
   const double step_inf = R.max1(step_part);

@@ -39,7 +39,7 @@ struct SolveParams {
   double *X, *U, *trace;
   int32_t* info;
   // scratch
-  double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Linv, *Lfac, *pmats, *gamma, *gammaw, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
+  double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Linv, *Lfac, *pmats, *gamma, *gammaw, *lbw, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
   int32_t *si, *pcg_iters;
   unsigned int* counters;  // [0] active count, [1] ticket, [2] pending solves, [3] passes run
 };
@@ -781,6 +781,13 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_schur(SolveParams P) {
     return;
   }
   warp_tri_inverse<NX>(S.W, S.spd, lane);   // S.W <- L^-1 (zeros above the diagonal)
+  {   // lbw_k = 1 / ||L_k^-1||_F^2 <= sigma_min(L_k)^2: ||L_k v||^2 >= lbw_k ||v||^2 (stop-test lower bound)
+    double f2 = 0.0;
+    for (int idx = lane; idx < NX * NX; idx += 32) f2 = fma(S.W[idx], S.W[idx], f2);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+    if (lane == 0) P.lbw[(size_t)b * nb + k] = 1.0 / f2;
+  }
   double* LiP = pm + (size_t)P.N * L::BSP + (size_t)k * L::TRP;
   double* LfP = LiP + (size_t)nb * L::TRP;
   double* Li = P.Linv + ((size_t)b * nb + k) * TRI;
