@@ -37,106 +37,12 @@ __global__ void k_init(SolveParams P) {
 
 
 // -----------------------------------------------------------------------------------------
-// k_update: per solve: first-minimum argmin over the candidates, strict-decrease accept test
-// (sqp.py:193-195), X += a dX, U += a dU (sqp.py:277-281), IterationRecord (sqp.py:283-292),
-// adapt_rho (sqp.py:198-201), budget termination; counts the still-active solves and, when
-// run inside the WHILE graph node, sets its condition.
+// k_update: update_solve as a kernel of its own (plain / profiled passes; the graph passes run it as
+// the tail of k_linesearch).
 // -----------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_update(SolveParams P, int nx, int nu, cudaGraphConditionalHandle cond,
                                                 int use_cond) {
-  const int b = blockIdx.x;
-  int32_t* si = P.si + b * SI_WORDS;
-  __shared__ double s_alpha;
-  __shared__ int s_accept;
-  const int active = si[SI_ACTIVE];
-  const int skip = si[SI_SKIP_LS];
-  if (skip == 2) {   // tolerance exit at the very first iteration: patch merit(X0, U0) into its record
-    if (threadIdx.x == 0) {
-      const double m0 = P.merits[(size_t)b * (P.C + 1) + P.C];
-      P.sd[b * SD_WORDS + SD_MERIT] = m0;
-      P.trace[((size_t)b * P.max_it + si[SI_IT]) * GATO_TRACE_WORDS + GATO_TRACE_MERIT] = m0;
-      si[SI_MERIT_VALID] = 1;
-      si[SI_SKIP_LS] = 1;
-    }
-  }
-  if (active && !skip) {
-    if (threadIdx.x == 0) {
-      const double* mer = P.merits + (size_t)b * (P.C + 1);
-      if (!si[SI_MERIT_VALID]) {
-        P.sd[b * SD_WORDS + SD_MERIT] = mer[P.C];
-        si[SI_MERIT_VALID] = 1;
-      }
-      int best = 0;
-      double bm = mer[0];
-      for (int c0 = 1; c0 < P.C; c0 += 8) {   // loads of a chunk issue together; first minimum wins
-        double m[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) m[i] = (c0 + i < P.C) ? mer[c0 + i] : INFINITY;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (c0 + i < P.C && m[i] < bm) {
-            bm = m[i];
-            best = c0 + i;
-          }
-      }
-      // np.argmin returns the first NaN if any; merits are never NaN (non-finite -> +inf)
-      const double cur = P.sd[b * SD_WORDS + SD_MERIT];
-      const int accepted = bm < cur;
-      const double alpha = P.alphas[best];
-      s_alpha = alpha;
-      s_accept = accepted;
-      double viol = P.sd[b * SD_WORDS + SD_VIOL];
-      double merit = cur;
-      if (accepted) {
-        merit = bm;
-        viol = P.viols[(size_t)b * (P.C + 1) + best];
-        P.sd[b * SD_WORDS + SD_MERIT] = bm;
-      }
-      const int it = si[SI_IT];
-      const double rho = P.sd[b * SD_WORDS + SD_RHO];
-      double* tr = P.trace + ((size_t)b * P.max_it + it) * GATO_TRACE_WORDS;
-      tr[GATO_TRACE_MERIT] = merit;
-      tr[GATO_TRACE_CONSTRAINT_L1] = viol;
-      tr[GATO_TRACE_ALPHA] = alpha;
-      tr[GATO_TRACE_RHO] = rho;
-      tr[GATO_TRACE_PCG_ITERATIONS] = (double)si[SI_PCG_ITS];
-      tr[GATO_TRACE_ACCEPTED] = accepted ? 1.0 : 0.0;
-      tr[GATO_TRACE_STEP_INF_NORM] = P.sd[b * SD_WORDS + SD_STEP_INF];
-      tr[GATO_TRACE_ITERATION] = (double)it;
-      const double nrho = accepted ? rho / P.rho_factor : rho * P.rho_factor;
-      P.sd[b * SD_WORDS + SD_RHO] = fmin(fmax(nrho, P.rho_min), P.rho_max);
-      int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
-      info[GATO_INFO_N_RECORDS] = it + 1;
-      si[SI_IT] = it + 1;
-      if (it + 1 >= P.max_it) si[SI_ACTIVE] = 0;
-    }
-    __syncthreads();
-    if (s_accept) {
-      const double alpha = s_alpha;
-      const int nX = (P.N + 1) * nx, nU = P.N * nu;
-      double* X = P.X + (size_t)b * nX;
-      const double* dX = P.dX + (size_t)b * nX;
-      for (int i = threadIdx.x; i < nX; i += blockDim.x) X[i] = __dadd_rn(X[i], __dmul_rn(alpha, dX[i]));
-      double* U = P.U + (size_t)b * nU;
-      const double* dU = P.dU + (size_t)b * nU;
-      for (int i = threadIdx.x; i < nU; i += blockDim.x) U[i] = __dadd_rn(U[i], __dmul_rn(alpha, dU[i]));
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int still = si[SI_ACTIVE];
-    if (still) atomicAdd(&P.counters[0], 1u);
-    __threadfence();
-    const unsigned ticket = atomicAdd(&P.counters[1], 1u);
-    if (ticket == gridDim.x - 1) {
-      __threadfence();
-      const unsigned n_active = atomicExch(&P.counters[0], 0u);
-      P.counters[1] = 0;
-      P.counters[2] = n_active;  // host-visible "pending" word
-      P.counters[3] += 1;        // passes executed
-      if (use_cond) cudaGraphSetConditional(cond, n_active > 0 ? 1u : 0u);
-    }
-  }
+  update_solve(P, blockIdx.x, nx, nu, cond, use_cond, gridDim.x);
 }
 
 // mpc.py:85-89: shift one knot left, duplicate the tail.  One CTA per solve.

@@ -320,8 +320,9 @@ __global__ void __launch_bounds__(kPcgRtMaxThreads, 1) k_pcg_rt(SolveParams P) {
   };
 
   int its = 0, breakdown = 0;
-  bool nan_curv = false, verify = false;
+  bool nan_curv = false, verify = false, exact = false;
   double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
+  const double lbw = valid ? P.lbw[(size_t)b * nb + k] : 0.0;
   const double2 s = R.sum2(g2, viol_part);
   const double viol = s.y;
   const double tol2 = P.pcg_tol * P.pcg_tol;
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(kPcgRtMaxThreads, 1) k_pcg_rt(SolveParams P) {
       p1 = valid ? r1 - t1 : 0.0;
     }
     double rz = R.sum1(r0 * p0 + r1 * p1);
+    double inv_rz = 1.0 / rz;
     const int cap = P.pcg_cap;
     for (int it = 1; it <= cap; ++it) {
       put(vp, p0, p1);
@@ -368,10 +370,15 @@ __global__ void __launch_bounds__(kPcgRtMaxThreads, 1) k_pcg_rt(SolveParams P) {
         offmv(vr, t0, t1);
         z0 = r0 - t0;
         z1 = r1 - t1;
-        n2 = lnorm2(vr);
+        // ||L r^||^2: exact once the lower bound sum_k lbw_k ||r^_k||^2 has dropped to tol^2
+        n2 = exact ? lnorm2(vr) : lbw * (r0 * r0 + r1 * r1);
       }
-      const double2 rr = R.sum2(r0 * z0 + r1 * z1, n2);
+      double2 rr = R.sum2(r0 * z0 + r1 * z1, n2);
       its = it;
+      if (!exact && rr.y <= tol2) {   // the bound no longer excludes convergence
+        exact = true;
+        rr.y = R.sum1(valid ? lnorm2(vr) : 0.0);
+      }
       if (verify || rr.y <= tol2) {
         // true residual L (gamma^ - lam^ - O^ lam^) of blocktri.py:165
         put(vp, l0, l1);
@@ -388,10 +395,11 @@ __global__ void __launch_bounds__(kPcgRtMaxThreads, 1) k_pcg_rt(SolveParams P) {
         if (sqrt(true2) <= P.pcg_tol) break;
         verify = true;
       }
-      const double beta = rr.x / rz;
+      const double beta = rr.x * inv_rz;   // 1 / rz was formed while the products ran
       p0 = z0 + beta * p0;
       p1 = z1 + beta * p1;
       rz = rr.x;
+      inv_rz = 1.0 / rz;
     }
   }
   if (nan_curv) l0 = l1 = nan("");

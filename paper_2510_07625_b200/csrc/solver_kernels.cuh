@@ -42,6 +42,10 @@ struct SolveParams {
   double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Linv, *Lfac, *pmats, *gamma, *gammaw, *lbw, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
   int32_t *si, *pcg_iters;
   unsigned int* counters;  // [0] active count, [1] ticket, [2] pending solves, [3] passes run
+  // fused tail of k_linesearch: its last CTA of a solve runs update_solve
+  unsigned int* ls_ticket;  // [M]
+  unsigned long long cond;  // cudaGraphConditionalHandle of the WHILE node
+  int use_cond, fuse_update;
 };
 
 // doubles per solve in hinv: [Qs^-1 | Qt^-1 | Rs^-1], padded to an even count (16-byte rows)
@@ -884,6 +888,108 @@ struct BlockReducer {
 };
 
 // -----------------------------------------------------------------------------------------
+// update_solve (one CTA per solve; k_update, or the last line-search CTA of the solve): first-minimum argmin over the candidates, strict-decrease accept test
+// (sqp.py:193-195), X += a dX, U += a dU (sqp.py:277-281), IterationRecord (sqp.py:283-292),
+// adapt_rho (sqp.py:198-201), budget termination; counts the still-active solves and, when
+// run inside the WHILE graph node, sets its condition.
+// -----------------------------------------------------------------------------------------
+__device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx, int nu,
+                                             cudaGraphConditionalHandle cond, int use_cond, unsigned n_solves) {
+  int32_t* si = P.si + b * SI_WORDS;
+  __shared__ double s_alpha;
+  __shared__ int s_accept;
+  const int active = si[SI_ACTIVE];
+  const int skip = si[SI_SKIP_LS];
+  if (skip == 2) {   // tolerance exit at the very first iteration: patch merit(X0, U0) into its record
+    if (threadIdx.x == 0) {
+      const double m0 = __ldcg(&P.merits[(size_t)b * (P.C + 1) + P.C]);
+      P.sd[b * SD_WORDS + SD_MERIT] = m0;
+      P.trace[((size_t)b * P.max_it + si[SI_IT]) * GATO_TRACE_WORDS + GATO_TRACE_MERIT] = m0;
+      si[SI_MERIT_VALID] = 1;
+      si[SI_SKIP_LS] = 1;
+    }
+  }
+  if (active && !skip) {
+    if (threadIdx.x == 0) {
+      const double* mer = P.merits + (size_t)b * (P.C + 1);
+      if (!si[SI_MERIT_VALID]) {
+        P.sd[b * SD_WORDS + SD_MERIT] = __ldcg(&mer[P.C]);
+        si[SI_MERIT_VALID] = 1;
+      }
+      int best = 0;
+      double bm = __ldcg(&mer[0]);
+      for (int c0 = 1; c0 < P.C; c0 += 8) {   // loads of a chunk issue together; first minimum wins
+        double m[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m[i] = (c0 + i < P.C) ? __ldcg(&mer[c0 + i]) : INFINITY;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (c0 + i < P.C && m[i] < bm) {
+            bm = m[i];
+            best = c0 + i;
+          }
+      }
+      // np.argmin returns the first NaN if any; merits are never NaN (non-finite -> +inf)
+      const double cur = P.sd[b * SD_WORDS + SD_MERIT];
+      const int accepted = bm < cur;
+      const double alpha = P.alphas[best];
+      s_alpha = alpha;
+      s_accept = accepted;
+      double viol = P.sd[b * SD_WORDS + SD_VIOL];
+      double merit = cur;
+      if (accepted) {
+        merit = bm;
+        viol = __ldcg(&P.viols[(size_t)b * (P.C + 1) + best]);
+        P.sd[b * SD_WORDS + SD_MERIT] = bm;
+      }
+      const int it = si[SI_IT];
+      const double rho = P.sd[b * SD_WORDS + SD_RHO];
+      double* tr = P.trace + ((size_t)b * P.max_it + it) * GATO_TRACE_WORDS;
+      tr[GATO_TRACE_MERIT] = merit;
+      tr[GATO_TRACE_CONSTRAINT_L1] = viol;
+      tr[GATO_TRACE_ALPHA] = alpha;
+      tr[GATO_TRACE_RHO] = rho;
+      tr[GATO_TRACE_PCG_ITERATIONS] = (double)si[SI_PCG_ITS];
+      tr[GATO_TRACE_ACCEPTED] = accepted ? 1.0 : 0.0;
+      tr[GATO_TRACE_STEP_INF_NORM] = P.sd[b * SD_WORDS + SD_STEP_INF];
+      tr[GATO_TRACE_ITERATION] = (double)it;
+      const double nrho = accepted ? rho / P.rho_factor : rho * P.rho_factor;
+      P.sd[b * SD_WORDS + SD_RHO] = fmin(fmax(nrho, P.rho_min), P.rho_max);
+      int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
+      info[GATO_INFO_N_RECORDS] = it + 1;
+      si[SI_IT] = it + 1;
+      if (it + 1 >= P.max_it) si[SI_ACTIVE] = 0;
+    }
+    __syncthreads();
+    if (s_accept) {
+      const double alpha = s_alpha;
+      const int nX = (P.N + 1) * nx, nU = P.N * nu;
+      double* X = P.X + (size_t)b * nX;
+      const double* dX = P.dX + (size_t)b * nX;
+      for (int i = threadIdx.x; i < nX; i += blockDim.x) X[i] = __dadd_rn(X[i], __dmul_rn(alpha, dX[i]));
+      double* U = P.U + (size_t)b * nU;
+      const double* dU = P.dU + (size_t)b * nU;
+      for (int i = threadIdx.x; i < nU; i += blockDim.x) U[i] = __dadd_rn(U[i], __dmul_rn(alpha, dU[i]));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int still = si[SI_ACTIVE];
+    if (still) atomicAdd(&P.counters[0], 1u);
+    __threadfence();
+    const unsigned ticket = atomicAdd(&P.counters[1], 1u);
+    if (ticket == n_solves - 1) {
+      __threadfence();
+      const unsigned n_active = atomicExch(&P.counters[0], 0u);
+      P.counters[1] = 0;
+      P.counters[2] = n_active;  // host-visible "pending" word
+      P.counters[3] += 1;        // passes executed
+      if (use_cond) cudaGraphSetConditional(cond, n_active > 0 ? 1u : 0u);
+    }
+  }
+}
+
+// -----------------------------------------------------------------------------------------
 // k_linesearch: merit of every candidate (sqp.py:132-166).  grid (C, M), one thread per stage
 // knot: candidate point (X + a dX, U + a dU), one RK4 prediction, |defect|_1, quadratic cost
 // with the undamped weights; fixed-tree reduction over knots.  Non-finite candidates -> +inf.
@@ -895,16 +1001,19 @@ __global__ void __launch_bounds__(128, MINB) k_linesearch(SolveParams P) {
   const int c = blockIdx.x, b = blockIdx.y;
   const int32_t* si = P.si + b * SI_WORDS;
   const int skip = si[SI_SKIP_LS];
+  bool run;
   if (c < P.C) {
-    if (!si[SI_ACTIVE] || skip) return;
+    run = si[SI_ACTIVE] && !skip;
   } else {
     // candidate C is the current iterate (alpha = 0): merit(X0, U0) of sqp.py:229, needed once
-    if (!((si[SI_ACTIVE] && !skip && !si[SI_MERIT_VALID]) || skip == 2)) return;
+    run = (si[SI_ACTIVE] && !skip && !si[SI_MERIT_VALID]) || skip == 2;
   }
+  if (!run && !P.fuse_update) return;
   __shared__ double2 red[2 * 32];
-  __shared__ int bad_flag;
+  __shared__ int bad_flag, is_last;
   if (threadIdx.x == 0) bad_flag = 0;
   __syncthreads();
+  if (run) {
   const int N = P.N, nb = N + 1;
   const double alpha = (c < P.C) ? P.alphas[c] : 0.0;
   double cost = 0.0, viol = 0.0;
@@ -980,6 +1089,21 @@ __global__ void __launch_bounds__(128, MINB) k_linesearch(SolveParams P) {
     if (bad_flag || !isfinite(value)) value = INFINITY;
     P.merits[(size_t)b * (P.C + 1) + c] = value;
     P.viols[(size_t)b * (P.C + 1) + c] = s.y;
+  }
+  }  // run
+  if (!P.fuse_update) return;
+  // the last CTA of this solve to get here applies the step (every candidate CTA takes a ticket,
+  // whether it evaluated a candidate or not)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned ticket = atomicAdd(&P.ls_ticket[b], 1u);
+    is_last = ticket == gridDim.x - 1;
+    if (is_last) P.ls_ticket[b] = 0;
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    update_solve(P, b, NX, NU, (cudaGraphConditionalHandle)P.cond, P.use_cond, gridDim.y);
   }
 }
 
