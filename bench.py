@@ -411,6 +411,9 @@ def run_gpu_arm(args, w, rank, local_rank, world):
         fam_ms = {"linearize": kern_ms["linearize"], "schur": kern_ms["schur"] + kern_ms["hessinv"],
                   "pcg": kern_ms["pcg"], "linesearch": kern_ms["linesearch"]}
         dominant = max(fam_ms, key=fam_ms.get)
+        # the PCG family runs the register-resident kernel at short horizons (model_ops.cuh: pcg_use_rt)
+        kernel_names = {"linearize": "k_lin_tangent_iiwa", "schur": "k_schur",
+                        "pcg": "k_pcg_rt" if (N + 1) * 7 <= 256 else "k_pcg", "linesearch": "k_linesearch"}
         launches_dom = K_sqp
         achieved = fam_flops[dominant] / (fam_ms[dominant] * 1e-3) / 1e12
         total_flops = float(np.sum([flops_solve_iteration(N, p) for p in P_prof.reshape(-1)]))
@@ -434,13 +437,11 @@ def run_gpu_arm(args, w, rank, local_rank, world):
             "gpu_launches_per_step": int(launches_per_step),
             "clocks": clocks.summary(),
             "roofline": {
-                "bound": "fp64", "kernel": {"linearize": "k_linearize_iiwa", "schur": "k_schur", "pcg": "k_pcg",
-                                            "linesearch": "k_linesearch"}[dominant],
+                "bound": "fp64", "kernel": kernel_names[dominant],
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                 "peak_source": "in-run DFMA probe (gato_measure_fp64_peak); MEASURED_PEAKS.json carries no fp64 figure",
                 "launch_ms": fam_ms[dominant] / launches_dom, "algorithmic_flops_per_launch": fam_flops[dominant] / launches_dom,
-                "traffic": ncu_traffic(args.workload, {"linearize": "k_lin_tangent_iiwa", "schur": "k_schur",
-                                                       "pcg": "k_pcg", "linesearch": "k_linesearch"}[dominant]),
+                "traffic": ncu_traffic(args.workload, kernel_names[dominant]),
                 "hbm": {"achieved": alg_bytes / (kern_ms["total"] * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                         "frac": alg_bytes / (kern_ms["total"] * 1e-3) / 1e9 / hbm_peak, "peak_source": hbm_src,
                         "algorithmic_bytes_per_step": alg_bytes},

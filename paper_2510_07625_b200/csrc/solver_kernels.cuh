@@ -560,14 +560,16 @@ struct PcgLayout {
 // diagonal part of form_preconditioner qpform.py:342-353):
 //   k = 0 : S_00 = Q_0^-1, gamma_0 = Q_0^-1 q_0 + (x_s - x_0)
 //   k > 0 : theta = A Q^-1 A^T + B R^-1 B^T + Q_k^-1, phi = -A Q^-1, gamma_k = zeta + e
-//   D_k^-1 = spd_inverse(S_kk).
-// The stair preconditioner's off-diagonal blocks -D_{k+1}^-1 phi_k D_k^-1 (qpform.py:355-356)
-// are never formed: k_pcg applies Phi^-1 in factored form, which needs no neighbour's D^-1
-// here and therefore no grid-wide synchronisation.
+//   S_kk = L_k L_k^T (Cholesky; a failing pivot is reported like spd_inverse's, qpform.py:352-353).
+// The stair preconditioner's blocks D_k^-1 and -D_{k+1}^-1 phi_k D_k^-1 (qpform.py:345-356) are never
+// formed: the PCG kernels work in the block-Jacobi-whitened variables (pcg_kernels.cuh), for which
+// this warp emits L_k, L_k^-1, W_{k-1} = L_k^-1 phi_{k-1}, gamma^_k = L_k^-1 gamma_k and the
+// stop-test weight 1 / ||L_k^-1||_F^2.  No neighbour's factor is needed here, hence no grid-wide
+// synchronisation.
 // Lane (r, half) computes a 1 x NX/2 strip of every product, with A^T and B^T staged so that
-// every shared-memory read is a row read.  Besides the plain arrays (Sdiag, Soff, Dinv: parity
+// every shared-memory read is a row read.  Besides the plain arrays (Sdiag, Soff, Linv, Lfac: parity
 // tests, step recovery) the warp writes its part of the padded per-solve matrix record that
-// k_pcg pulls into shared memory with one bulk copy.
+// the PCG kernels pull into shared memory with bulk copies.
 // -----------------------------------------------------------------------------------------
 template <int NX, int NU>
 struct SchurSmem {
