@@ -62,45 +62,65 @@ __device__ __forceinline__ int tri_idx(int i, int j) { return i >= j ? i * (i + 
 // -----------------------------------------------------------------------------------------
 template <int D>
 struct SpdScratch {
-  double L[D * (D + 1)];      // factor, row stride D + 1 (odd for even D: conflict-free rows)
-  double invd[D + (D & 1)];   // reciprocals of the factor's diagonal
+  double L[D * (D + 1)];         // factor, row stride D + 1 (odd for even D: conflict-free rows)
+  double invd[D + (D & 1)];      // reciprocals of the factor's diagonal
+  double col[2][D + (D & 1)];    // the pivot column being eliminated, double buffered
 };
 
-// lower Cholesky factor of the D*D matrix in W -> S.L (row stride D + 1), S.invd; returns 0 or the
-// 1-based index of the failing pivot
+// lower Cholesky factor of the D*D matrix in W -> S.L (row stride D + 1, lower triangle), S.invd;
+// returns 0 or the 1-based index of the failing pivot (dpotrf semantics: pivot <= 0 or NaN).
+// Right-looking, the lower triangle lives in REGISTERS spread over the 32 lanes (entry p = lane + 32 e
+// of the packed triangle): per pivot one shuffle broadcasts the diagonal, every lane forms sqrt and
+// rsqrt itself, the owners publish the scaled column through shared memory (one __syncwarp) and each
+// lane updates the entries it owns -- no index arithmetic inside the pivot loop.
 template <int D>
 __device__ __forceinline__ int warp_cholesky(const double* W, SpdScratch<D>& S, int lane) {
-  constexpr int LD = D + 1;
-  for (int idx = lane; idx < D * D; idx += 32) S.L[(idx / D) * LD + idx % D] = W[idx];
-  __syncwarp();
+  constexpr int LD = D + 1, TRI = D * (D + 1) / 2, E = (TRI + 31) / 32;
+  int ei[E], ek[E];
+  double a[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int p = lane + 32 * e;
+    int i = 0;
+    while ((i + 1) * (i + 2) / 2 <= p) ++i;
+    const int k = p - i * (i + 1) / 2;
+    const bool ok = p < TRI;
+    ei[e] = ok ? i : -1;
+    ek[e] = ok ? k : -1;
+    a[e] = ok ? W[i * D + k] : 0.0;
+  }
   int fail = 0;
+#pragma unroll
   for (int j = 0; j < D; ++j) {
-    const double d = S.L[j * LD + j];
-    if (!(d > 0.0)) {   // dpotrf: pivot <= 0 or NaN
+    const int pj = j * (j + 1) / 2 + j;
+    const double d = __shfl_sync(0xffffffffu, a[pj >> 5], pj & 31);
+    if (!(d > 0.0)) {
       fail = j + 1;
       break;
     }
-    const double r = sqrt(d), ir = 1.0 / r;
-    __syncwarp();
-    if (lane == j) {
-      S.L[j * LD + j] = r;
-      S.invd[j] = ir;
+    const double r = sqrt(d), ir = rsqrt(d);
+    double* col = S.col[j & 1];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (ek[e] == j) {
+        a[e] = (ei[e] == j) ? r : a[e] * ir;
+        col[ei[e]] = a[e];
+      }
     }
-    if (lane > j && lane < D) S.L[lane * LD + j] = S.L[lane * LD + j] * ir;
+    if (lane == 0) S.invd[j] = ir;
     __syncwarp();
-    // trailing update of the lower triangle, (i, k) pairs spread over the 32 lanes
-    const int rem = D - j - 1;
-    for (int pidx = lane; pidx < rem * (rem + 1) / 2; pidx += 32) {
-      int ii = (int)((sqrtf(8.0f * pidx + 1.0f) - 1.0f) * 0.5f);
-      while ((ii + 1) * (ii + 2) / 2 <= pidx) ++ii;
-      while (ii * (ii + 1) / 2 > pidx) --ii;
-      const int kk = pidx - ii * (ii + 1) / 2;
-      const int i = j + 1 + ii, k = j + 1 + kk;
-      S.L[i * LD + k] = fma(-S.L[i * LD + j], S.L[k * LD + j], S.L[i * LD + k]);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (ek[e] > j) a[e] = fma(-col[ei[e]], col[ek[e]], a[e]);
     }
-    __syncwarp();
   }
-  return fail;
+  if (fail) return fail;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (ek[e] >= 0) S.L[ei[e] * LD + ek[e]] = a[e];
+  }
+  __syncwarp();
+  return 0;
 }
 
 template <int D>
@@ -142,21 +162,22 @@ __device__ __forceinline__ int warp_spd_inverse(double* W, SpdScratch<D>& S, int
 }
 
 // W (D*D, row-major) <- L^-1 for the factor held in S (lower triangular, zeros above the diagonal):
-// lane c solves L y = e_c for column c.
+// lane c forms column c by right-looking forward substitution (every lane reads the same L entry:
+// broadcast loads; the serial chain is one multiply + one FMA per row).
 template <int D>
 __device__ __forceinline__ void warp_tri_inverse(double* W, const SpdScratch<D>& S, int lane) {
   constexpr int LD = D + 1;
   if (lane < D) {
-    double y[D];
+    double s[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) s[i] = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      double t = (i == lane) ? 1.0 : 0.0;
+      const double y = (i < lane) ? 0.0 : s[i] * S.invd[i];
+      W[i * D + lane] = y;
 #pragma unroll
-      for (int k = 0; k < i; ++k) t = fma(-S.L[i * LD + k], y[k], t);
-      y[i] = (i < lane) ? 0.0 : t * S.invd[i];
+      for (int m = i + 1; m < D; ++m) s[m] = fma(-S.L[m * LD + i], y, s[m]);
     }
-#pragma unroll
-    for (int i = 0; i < D; ++i) W[i * D + lane] = y[i];
   }
   __syncwarp();
 }
