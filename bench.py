@@ -340,17 +340,13 @@ def run_gpu_arm(args, w, rank, local_rank, world):
     h2d_bytes = sum(getattr(step_inputs, f).nbytes for f in h2d_fields)
 
     def e2e_step(s):
+        # BatchEngine.step = one gato_solve_host call: pinned H2D of the inputs, (device shift,) solve, D2H
         if track:
             step_inputs.goal[...] = ref_path[s:s + N + 1][None]
-            eng.upload(step_inputs, fields=h2d_fields)
-            eng.shift_warm_start()
-        else:
-            eng.upload(step_inputs, fields=h2d_fields)
-        eng.launch()
-        eng.finish()
-        out = eng.download()
-        if track:
+            out = eng.step(step_inputs, fields=h2d_fields, shift=True)
             step_inputs.x_start[...] = out.X[:, 1, :]      # "measured" state for the next control step
+        else:
+            out = eng.step(step_inputs, fields=h2d_fields)
         return out
 
     for s in range(min(args.warmup, 5)):

@@ -10,6 +10,8 @@
  *   gato_step_jacobians_many                  replaces dynamics.step_jacobians_many dynamics.py:774-802
  *   gato_pcg_batched                          replaces blocktri.pcg / btmv          blocktri.py:105-173
  *   gato_shift_warm_start                     replaces mpc.shift_warm_start         mpc.py:85-89
+ *   gato_best_of_batch                        replaces the best-of-batch argmin     mpc.py:283-298
+ *   gato_solve_host                           one control step of _MpcEngine.advance mpc.py:240-274
  *
  * The reference is pure Python and has no FFI of its own; INTEGRATION.md shows the ctypes
  * stub a maintainer would add to trajbatch/batch.py to call this library.
@@ -134,6 +136,17 @@ int gato_bind(gato_handle* h, const gato_buffers* bufs);
 int gato_solve(gato_handle* h, void* stream);
 /* X <- [X[1:], X[-1]], U <- [U[1:], U[-1]] for every solve, in place (mpc.py:85-89). */
 int gato_shift_warm_start(gato_handle* h, void* stream);
+/* One control step with HOST buffers in a single call (the MPC caller's inner loop, mpc.py:240-274):
+ * copy `in_bytes` from (pinned) host memory to `dev_in`, optionally shift the warm start, run the
+ * solve to termination, copy `out_bytes` from `dev_out` back to host memory and synchronise the
+ * stream. dev_in / dev_out are caller-owned device addresses (typically spans of the buffers bound
+ * with gato_bind); either copy may be skipped with 0 bytes. */
+int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host_in, int64_t in_bytes,
+                    int32_t shift_first, const void* dev_out, void* host_out, int64_t out_bytes);
+/* Best-of-batch selection on the device (mpc.py:283-298): index of the solve with the lowest final
+ * merit among the solves without a failure status, first minimum on ties, -1 if every solve failed;
+ * written to the device words *best_index / *best_merit (either may be null). Asynchronous. */
+int gato_best_of_batch(gato_handle* h, void* stream, int32_t* best_index, double* best_merit);
 /* Loop modes 2/3 enqueue exactly max_sqp_iterations passes; a PCG-breakdown retry (sqp.py:240-248)
  * consumes a pass without advancing its solve. gato_pending synchronises the stream and reports
  * how many solves are still active; gato_resume enqueues further passes. In loop mode 1 (WHILE

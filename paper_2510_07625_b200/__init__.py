@@ -6,7 +6,7 @@ Public surface mirrors the hot-path names of the reference package ``trajbatch``
 kernels behind the C ABI in include/gato_b200.h.  There is no CPU execution path.
 """
 
-from .batch import BatchSpec, batch_solve, clear_engine_cache, shard_bounds, sqp_solve
+from .batch import BatchSpec, batch_solve, bench_scaling, clear_engine_cache, shard_bounds, sqp_solve
 from .engine import BatchEngine, PackedBatch, PackedResult, pcg_batched, step_jacobians_many, step_many
 from .errors import (BackendUnavailableError, ConfigError, DimensionError, FactorizationError,
                      PcgBreakdownError)
@@ -22,6 +22,6 @@ __all__ = [
     "CostSpec", "DimensionError", "DoubleIntegrator", "DynamicsModel", "ExternalForce",
     "FactorizationError", "Iiwa14", "IterationRecord", "LineSearchSettings", "PackedBatch",
     "PackedResult", "PcgBreakdownError", "PcgSettings", "Pendulum", "ProblemSpec", "SolverSettings",
-    "SqpResult", "TwoLinkArm", "batch_solve", "clear_engine_cache", "pcg_batched", "shard_bounds",
+    "SqpResult", "TwoLinkArm", "batch_solve", "bench_scaling", "clear_engine_cache", "pcg_batched", "shard_bounds",
     "sqp_solve", "step_jacobians_many", "step_many",
 ]

@@ -253,3 +253,42 @@ def sqp_solve(problem: ProblemSpec, X_init, U_init, settings: SolverSettings | N
             raise FactorizationError(msg, int(res.info[0, _lib.INFO_FAIL_KNOT]))
         raise PcgBreakdownError(msg, int(res.info[0, _lib.INFO_FAIL_AUX]))
     return unpack_results(res)[0][0]
+
+
+def bench_scaling(problem_template: ProblemSpec, M_list, N_list, workers: int = 1, repeats: int = 3,
+                  budget_iterations: int = 5, devices: list[int] | None = None) -> list[dict]:
+    """Median/p90 wall times over an (M, N) grid of fixed-budget batches: the reference's
+    ``bench_scaling`` (batch.py:127-169) with the same protocol -- M copies of the template resized
+    to horizon N, zero initialisation, exactly ``budget_iterations`` SQP iterations, one warm-up per
+    cell discarded -- and the same row schema (M, N, median_ms, p90_ms, workers), so the reference's
+    table / heat-map tooling (cli.py:264-280) consumes the rows unchanged.  Extra columns:
+    ``device_ms`` (CUDA-event time of the batch), ``sqp_iteration_rate_hz`` and
+    ``solve_iterations_per_s`` derived from it."""
+    import dataclasses
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    if repeats < 1:
+        raise ValueError("repeats must be >= 1")
+    if np.asarray(problem_template.cost.goal).ndim != 1:
+        raise ValueError("bench_scaling needs a template with a single-state goal")
+    settings = SolverSettings(max_sqp_iterations=budget_iterations, step_tolerance=None)
+    rows = []
+    for N in N_list:
+        problem = dataclasses.replace(problem_template, horizon=int(N))
+        n, m = problem.model.state_dim, problem.model.control_dim
+        init = (np.zeros((N + 1, n)), np.zeros((N, m)))
+        for M in M_list:
+            spec = BatchSpec([problem] * M, [init] * M, settings)
+            batch_solve(spec, workers=workers, devices=devices)          # warm-up discarded
+            runs = [batch_solve(spec, workers=workers, devices=devices) for _ in range(repeats)]
+            times = sorted(r.wall_time for r in runs)
+            median = times[len(times) // 2] if repeats % 2 else 0.5 * (times[len(times) // 2 - 1] + times[len(times) // 2])
+            p90 = times[min(len(times) - 1, int(np.ceil(0.9 * len(times))) - 1)]
+            dev = float(np.median([r.device_time for r in runs]))
+            rows.append({
+                "M": M, "N": N, "median_ms": 1e3 * median, "p90_ms": 1e3 * p90, "workers": workers,
+                "device_ms": 1e3 * dev,
+                "sqp_iteration_rate_hz": budget_iterations / dev if dev > 0 else float("nan"),
+                "solve_iterations_per_s": M * budget_iterations / dev if dev > 0 else float("nan"),
+            })
+    return rows

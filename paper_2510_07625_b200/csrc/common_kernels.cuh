@@ -45,6 +45,45 @@ __global__ void __launch_bounds__(128) k_update(SolveParams P, int nx, int nu, c
   update_solve(P, blockIdx.x, nx, nu, cond, use_cond, gridDim.x);
 }
 
+// mpc.py:283-298: argmin of the final merit over the solves that did not fail, first minimum on ties.
+// One CTA; (merit, index) pairs compared lexicographically so the result does not depend on the
+// reduction order.
+__global__ void __launch_bounds__(256) k_best_of_batch(SolveParams P, int32_t* best_index, double* best_merit) {
+  __shared__ double s_m[256];
+  __shared__ int s_i[256];
+  double bm = INFINITY;
+  int bi = INT_MAX;
+  for (int b = threadIdx.x; b < P.M; b += blockDim.x) {
+    if (P.info[(size_t)b * GATO_INFO_WORDS + GATO_INFO_STATUS] != GATO_STATUS_OK) continue;
+    const double m = P.sd[b * SD_WORDS + SD_MERIT];
+    if (bi == INT_MAX || m < bm) {   // ascending b within a thread: first minimum kept
+      bm = m;
+      bi = b;
+    }
+  }
+  s_m[threadIdx.x] = bm;
+  s_i[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double m2 = s_m[threadIdx.x + o];
+      const int i2 = s_i[threadIdx.x + o];
+      const double m1 = s_m[threadIdx.x];
+      const int i1 = s_i[threadIdx.x];
+      const bool take = i2 != INT_MAX && (i1 == INT_MAX || m2 < m1 || (m2 == m1 && i2 < i1));
+      if (take) {
+        s_m[threadIdx.x] = m2;
+        s_i[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (best_index) *best_index = s_i[0] == INT_MAX ? -1 : s_i[0];
+    if (best_merit) *best_merit = s_m[0];
+  }
+}
+
 // mpc.py:85-89: shift one knot left, duplicate the tail.  One CTA per solve.
 __global__ void k_shift(double* X, double* U, int N, int nx, int nu) {
   extern __shared__ double sh[];

@@ -410,6 +410,47 @@ int gato_shift_warm_start(gato_handle* h, void* stream) {
   return GATO_OK;
 }
 
+int gato_best_of_batch(gato_handle* h, void* stream, int32_t* best_index, double* best_merit) {
+  if (!h || !h->bound) return GATO_E_INVALID;
+  k_best_of_batch<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(h->P, best_index, best_merit);
+  CK(cudaGetLastError());
+  return GATO_OK;
+}
+
+int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host_in, int64_t in_bytes,
+                    int32_t shift_first, const void* dev_out, void* host_out, int64_t out_bytes) {
+  if (!h) return GATO_E_INVALID;
+  if (!h->bound) {
+    set_error(h, "gato_solve_host before gato_bind");
+    return GATO_E_UNBOUND;
+  }
+  if (in_bytes < 0 || out_bytes < 0 || (in_bytes > 0 && (!dev_in || !host_in)) ||
+      (out_bytes > 0 && (!dev_out || !host_out))) {
+    set_error(h, "gato_solve_host: null buffer with a non-zero size");
+    return GATO_E_INVALID;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (in_bytes > 0) CK(cudaMemcpyAsync(dev_in, host_in, (size_t)in_bytes, cudaMemcpyHostToDevice, s));
+  int rc = GATO_OK;
+  if (shift_first) rc = gato_shift_warm_start(h, stream);
+  if (rc == GATO_OK) rc = gato_solve(h, stream);
+  if (rc != GATO_OK) return rc;
+  if (h->loop_mode != 1) {   // no device-side WHILE: a PCG retry may have used up a pass
+    int guard = h->cfg.max_sqp_iterations * (h->cfg.pcg_retry_limit + 1) + 1;
+    int32_t pending = 0;
+    while (guard-- > 0) {
+      rc = gato_pending(h, stream, &pending);
+      if (rc != GATO_OK) return rc;
+      if (pending == 0) break;
+      rc = gato_resume(h, stream, 1);
+      if (rc != GATO_OK) return rc;
+    }
+  }
+  if (out_bytes > 0) CK(cudaMemcpyAsync(host_out, dev_out, (size_t)out_bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return GATO_OK;
+}
+
 int gato_scratch(gato_handle* h, const char* name, void** dev_ptr, int64_t* count) {
   if (!h || !name || !dev_ptr) return GATO_E_INVALID;
   for (const Scratch& s : h->scratch) {

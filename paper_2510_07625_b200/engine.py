@@ -249,6 +249,51 @@ class BatchEngine:
         self.finish()
         return self.download()
 
+    STEP_FIELDS = ("x_start", "goal", "force")
+
+    def step(self, batch: PackedBatch, fields=STEP_FIELDS, shift: bool = False, copy: bool = True) -> PackedResult:
+        """One control step with host buffers in ONE call across the C ABI (gato_solve_host): the named
+        inputs (a contiguous run of the arena; default: the per-step MPC inputs x_start, goal, force) go
+        host -> pinned -> device, the warm start is optionally shifted on the device (mpc.py:85-89), the
+        solve runs to termination and X, U, trace, info come back.  copy=False returns views of the
+        pinned mirror, valid until the next call."""
+        for name in fields:
+            src = getattr(batch, name)
+            if src.shape != self.shapes[name]:
+                raise ValueError(f"{name}: expected shape {self.shapes[name]}, got {src.shape}")
+            self.pin_np[name][...] = src
+        order = [n for n in self.layout if n in fields]
+        idx = [self.layout.index(n) for n in order]
+        if idx != list(range(idx[0], idx[0] + len(idx))):
+            raise ValueError("step(): the uploaded fields must be adjacent in the arena; use upload() + launch()")
+        cin, cout = self._span(order[0], order[-1]), self._span("X", "info")
+        base_d, base_h = self.arena.data_ptr(), self.pinned.data_ptr()
+        self._check(self.lib.gato_solve_host(
+            self.handle, C.c_void_p(self.stream.cuda_stream),
+            C.c_void_p(base_d + 8 * cin.start), C.c_void_p(base_h + 8 * cin.start), 8 * (cin.stop - cin.start),
+            1 if shift else 0,
+            C.c_void_p(base_d + 8 * cout.start), C.c_void_p(base_h + 8 * cout.start), 8 * (cout.stop - cout.start)),
+            "gato_solve_host")
+        get = (lambda a: a.copy()) if copy else (lambda a: a)
+        return PackedResult(get(self.pin_np["X"]), get(self.pin_np["U"]), get(self.pin_np["trace"]),
+                            get(self.pin_np["info"]), float("nan"))
+
+    def best_of_batch(self) -> tuple[int, float]:
+        """(index, final merit) of the best solve of the last batch, selected on the device
+        (gato_best_of_batch; mpc.py:283-298): lowest final merit among the solves that did not fail,
+        first minimum on ties; index -1 if every solve failed."""
+        torch = self.torch
+        with torch.cuda.device(self.device):
+            if not hasattr(self, "_best"):
+                self._best = (torch.zeros(1, dtype=torch.int32, device=self.device),
+                              torch.zeros(1, dtype=torch.float64, device=self.device))
+            bi, bm = self._best
+            self._check(self.lib.gato_best_of_batch(self.handle, C.c_void_p(self.stream.cuda_stream),
+                                                    C.c_void_p(bi.data_ptr()), C.c_void_p(bm.data_ptr())),
+                        "gato_best_of_batch")
+            self.stream.synchronize()
+            return int(bi.item()), float(bm.item())
+
     def shift_warm_start(self):
         """X, U <- shifted one knot left with the tail duplicated, on the device (mpc.py:85-89)."""
         self._check(self.lib.gato_shift_warm_start(self.handle, C.c_void_p(self.stream.cuda_stream)),

@@ -1,0 +1,106 @@
+"""The caller-side rows of the hot path on the GPU: one control step through
+a single C-ABI call (gato_solve_host), best-of-batch selection on the device (mpc.py:283-298) and the
+reference's bench_scaling protocol (batch.py:127-169)."""
+
+import numpy as np
+import pytest
+
+import paper_2510_07625_b200 as gb
+from paper_2510_07625_b200 import _lib, mpc, workloads
+from paper_2510_07625_b200.engine import INPUT_FIELDS
+
+pytestmark = pytest.mark.gpu
+
+
+def test_step_is_bitwise_the_staged_solve():
+    M, N = 6, 12
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    st = workloads.fixed_budget_settings(2)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, st)
+    try:
+        staged = eng.solve(batch)
+        fused = eng.step(batch, fields=INPUT_FIELDS)
+        view = eng.step(batch, fields=INPUT_FIELDS, copy=False)
+        assert view.X.base is not None     # a view of the pinned mirror, not a copy
+    finally:
+        eng.close()
+    for name in ("X", "U", "trace", "info"):
+        assert np.array_equal(getattr(staged, name), getattr(fused, name), equal_nan=name == "trace"), name
+        assert np.array_equal(getattr(staged, name), getattr(view, name), equal_nan=name == "trace"), name
+
+
+def test_mpc_step_with_device_shift_matches_host_shift():
+    """upload(x_start, goal, force) + device shift + solve in one call == the same control step
+    assembled on the host with mpc.shift_warm_start (mpc.py:85-89)."""
+    M, N = 4, 10
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    st = workloads.fixed_budget_settings(1)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, st)
+    try:
+        first = eng.solve(batch)
+        nxt = gb.PackedBatch(first.X[:, 1, :].copy(), batch.goal, batch.Q, batch.R, batch.QN, batch.force,
+                             batch.rho_init, batch.X, batch.U)
+        stepped = eng.step(nxt, shift=True)            # X, U stay on the device and are shifted there
+        Xs = np.concatenate([first.X[:, 1:], first.X[:, -1:]], axis=1)
+        Us = np.concatenate([first.U[:, 1:], first.U[:, -1:]], axis=1)
+        host = eng.solve(gb.PackedBatch(nxt.x_start, batch.goal, batch.Q, batch.R, batch.QN, batch.force,
+                                        batch.rho_init, Xs, Us))
+    finally:
+        eng.close()
+    assert np.array_equal(stepped.X, host.X) and np.array_equal(stepped.U, host.U)
+    assert np.array_equal(stepped.trace, host.trace, equal_nan=True)
+
+
+def test_step_rejects_scattered_fields():
+    M, N = 2, 4
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, workloads.fixed_budget_settings(1))
+    try:
+        with pytest.raises(ValueError):
+            eng.step(batch, fields=("x_start", "Q"))
+    finally:
+        eng.close()
+
+
+def test_best_of_batch_on_device_matches_the_host_rule():
+    """Nested rho grid (mpc.py:61-78) over copies of one problem: the device argmin picks what
+    mpc.best_of_batch picks from the unpacked results, and a failed slot is skipped."""
+    from paper_2510_07625_b200.batch import pack_problems, unpack_results
+    N = 16
+    cost = gb.CostSpec(Q=np.diag([1.0, 0.1]), R=np.diag([0.01]), QN=np.diag([100.0, 10.0]),
+                       goal=np.array([np.pi, 0.0]))
+    problem = gb.ProblemSpec(model=gb.Pendulum(), cost=cost, horizon=N, timestep=0.05, x_start=np.zeros(2))
+    bad = gb.ProblemSpec(model=gb.Pendulum(), cost=gb.CostSpec(Q=-100.0 * np.eye(2), R=np.diag([0.01]), QN=np.eye(2),
+                                                               goal=np.array([np.pi, 0.0])),
+                         horizon=N, timestep=0.05, x_start=np.zeros(2))
+    M = 9
+    rhos = mpc.rho_grid(M)
+    problems = [problem] * (M - 1) + [bad]
+    inits = [(np.zeros((N + 1, 2)), np.zeros((N, 1)))] * M
+    st = gb.SolverSettings(max_sqp_iterations=6, step_tolerance=None)
+    eng = gb.BatchEngine(gb.Pendulum(), M, N, 0.05, st)
+    try:
+        res = eng.solve(pack_problems(problems, inits, list(rhos)))
+        idx, merit = eng.best_of_batch()
+    finally:
+        eng.close()
+    results, errors = unpack_results(res)
+    assert errors[-1] is not None and "FactorizationError" in errors[-1]
+    want = mpc.best_of_batch(results)
+    assert idx == want and idx != M - 1
+    assert merit == results[want].final_merit
+
+
+def test_bench_scaling_rows_follow_the_reference_schema():
+    cost = gb.CostSpec(Q=np.eye(2), R=0.1 * np.eye(1), QN=10.0 * np.eye(2), goal=np.array([np.pi, 0.0]))
+    template = gb.ProblemSpec(model=gb.Pendulum(), cost=cost, horizon=8, timestep=0.05, x_start=np.zeros(2))
+    rows = gb.bench_scaling(template, [1, 4], [8, 16], workers=1, repeats=3, budget_iterations=2)
+    assert [(r["M"], r["N"]) for r in rows] == [(1, 8), (4, 8), (1, 16), (4, 16)]     # N outer, M inner
+    for r in rows:
+        assert list(r)[:5] == ["M", "N", "median_ms", "p90_ms", "workers"]             # batch.py:161-167
+        assert r["p90_ms"] >= r["median_ms"] > 0 and r["workers"] == 1
+        assert r["device_ms"] > 0 and r["solve_iterations_per_s"] > 0
+    with pytest.raises(ValueError):
+        gb.bench_scaling(gb.ProblemSpec(model=gb.Pendulum(), cost=gb.CostSpec(
+            Q=np.eye(2), R=0.1 * np.eye(1), QN=np.eye(2), goal=np.zeros((9, 2))), horizon=8, timestep=0.05,
+            x_start=np.zeros(2)), [1], [8])
