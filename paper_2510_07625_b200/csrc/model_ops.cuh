@@ -57,9 +57,10 @@ cudaError_t launch_linearize(const RowView& V, const ModelParams& mp, double h, 
       static int minb = 0;
       if (!minb) minb = env_int("GATO_TAN_MINB", 2);
       const unsigned grid = (unsigned)((rows + kLinKnotsPerCta - 1) / kLinKnotsPerCta);
-      if (minb == 3) k_lin_tangent_iiwa<3><<<grid, 128, 0, s>>>(V, h, rows, stages, A, B);
-      else if (minb == 4) k_lin_tangent_iiwa<4><<<grid, 128, 0, s>>>(V, h, rows, stages, A, B);
-      else k_lin_tangent_iiwa<2><<<grid, 128, 0, s>>>(V, h, rows, stages, A, B);
+      constexpr size_t tan_smem = (size_t)kLinKnotsPerCta * 4 * sizeof(iiwa::Stage);   // 34 KB
+      if (minb == 3) k_lin_tangent_iiwa<3><<<grid, 128, tan_smem, s>>>(V, h, rows, stages, A, B);
+      else if (minb == 4) k_lin_tangent_iiwa<4><<<grid, 128, tan_smem, s>>>(V, h, rows, stages, A, B);
+      else k_lin_tangent_iiwa<2><<<grid, 128, tan_smem, s>>>(V, h, rows, stages, A, B);
     }
   }
   return cudaGetLastError();

@@ -85,38 +85,6 @@ __device__ __forceinline__ void pcg_finish(const SolveParams& P, int b, int32_t*
   }
 }
 
-// one elected thread pulls `bytes` (multiple of 16) from global into shared memory with bulk async
-// copies (TMA, SASS UBLKCP) whose completion is counted in bytes on an mbarrier
-__device__ __forceinline__ void bulk_fill_issue(unsigned bar, void* dst_smem, const void* src, unsigned bytes) {
-  unsigned dst = (unsigned)__cvta_generic_to_shared(dst_smem);
-  const char* s = reinterpret_cast<const char*>(src);
-  constexpr unsigned CHUNK = 32768;
-  for (unsigned off = 0; off < bytes; off += CHUNK) {
-    const unsigned n = bytes - off < CHUNK ? bytes - off : CHUNK;
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     dst + off),
-                 "l"(s + off), "r"(n), "r"(bar)
-                 : "memory");
-  }
-}
-__device__ __forceinline__ void mbar_init(unsigned bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait0(unsigned bar) {
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(bar)
-        : "memory");
-  }
-}
-
 // CTA-wide sums with at most 8 warps: xor-shuffle tree, one barrier, fixed tree over the warps
 struct Reducer8 {
   double2* red;  // [2][8], zero-initialised (slots of absent warps stay zero)

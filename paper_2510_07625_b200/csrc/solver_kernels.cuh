@@ -235,6 +235,38 @@ __global__ void __launch_bounds__(96) k_hessinv(SolveParams P) {
   }
 }
 
+// one elected thread pulls `bytes` (multiple of 16) from global into shared memory with bulk async
+// copies (TMA, SASS UBLKCP) whose completion is counted in bytes on an mbarrier
+__device__ __forceinline__ void bulk_fill_issue(unsigned bar, void* dst_smem, const void* src, unsigned bytes) {
+  unsigned dst = (unsigned)__cvta_generic_to_shared(dst_smem);
+  const char* s = reinterpret_cast<const char*>(src);
+  constexpr unsigned CHUNK = 32768;
+  for (unsigned off = 0; off < bytes; off += CHUNK) {
+    const unsigned n = bytes - off < CHUNK ? bytes - off : CHUNK;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst + off),
+                 "l"(s + off), "r"(n), "r"(bar)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_init(unsigned bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(unsigned bar) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar)
+        : "memory");
+  }
+}
+
 // -----------------------------------------------------------------------------------------
 // Row addressing shared by the solve (row r = solve b, knot k) and the stateless operator
 // entry points (M = 1, N = rows): X has N+1 rows per solve, U and F have N.
@@ -502,16 +534,32 @@ __global__ void __launch_bounds__(128, MINB) k_lin_tangent_iiwa(RowView V, doubl
                                                           double* __restrict__ A, double* __restrict__ B) {
   constexpr int NX = 14, NU = 7, NF = 3;
   const int t = threadIdx.x;
-  if (t >= kLinKnotsPerCta * kLinDirs) return;
-  const int64_t r = (int64_t)blockIdx.x * kLinKnotsPerCta + t / kLinDirs;
+  // the CTA's stage records (consecutive knots: one contiguous span) come into shared memory with one
+  // bulk async copy (TMA); every thread of a knot then reads the same record at shared-memory latency
+  extern __shared__ __align__(16) unsigned char tan_smem[];
+  __shared__ __align__(8) unsigned long long tan_bar;
+  const int64_t r_first = (int64_t)blockIdx.x * kLinKnotsPerCta;
+  const int64_t r_left = rows - r_first;
+  const unsigned n_here = (unsigned)(r_left < kLinKnotsPerCta ? r_left : kLinKnotsPerCta);
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&tan_bar);
+  if (t == 0) mbar_init(bar);
+  __syncthreads();
+  if (t == 0) {
+    const unsigned bytes = n_here * 4u * (unsigned)sizeof(iiwa::Stage);
+    mbar_expect(bar, bytes);
+    bulk_fill_issue(bar, tan_smem, stages + r_first * 4, bytes);
+  }
+  const int64_t r = r_first + t / kLinDirs;
   const int d = t % kLinDirs;
-  if (r >= rows) return;
-  if (V.si && !V.si[(r / V.N) * SI_WORDS + SI_ACTIVE]) return;
+  const bool work = t < kLinKnotsPerCta * kLinDirs && r < rows &&
+                    !(V.si && !V.si[(r / V.N) * SI_WORDS + SI_ACTIVE]);
   double f[NF];
 #pragma unroll
-  for (int i = 0; i < NF; ++i) f[i] = V.F[r * NF + i];
+  for (int i = 0; i < NF; ++i) f[i] = work ? V.F[r * NF + i] : 0.0;
+  mbar_wait0(bar);   // also by the threads without work: nobody leaves while the copy is in flight
+  if (!work) return;
   const int du = (d >= NX) ? d - NX : -1;
-  const iiwa::Stage* st = stages + r * 4;
+  const iiwa::Stage* st = reinterpret_cast<const iiwa::Stage*>(tan_smem) + (t / kLinDirs) * 4;
   double dx[NX], dk[NX], acc[NX];
 #pragma unroll
   for (int i = 0; i < NX; ++i) {

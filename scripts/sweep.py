@@ -25,8 +25,16 @@ def main():
     ap.add_argument("--max-batch", type=int, default=512)
     ap.add_argument("--repeats", type=int, default=5)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--cpu", action="store_true",
+                    help="add the CPU reference port (oracle, forked pool over all host cores): one wave of "
+                         "min(M, cores) solves is timed per horizon and scaled by ceil(M / cores) waves "
+                         "(SURVEY.md 8d: prefix + linear scaling for cells that would take minutes)")
     args = ap.parse_args()
-    rows = ["M,N,median_ms,p90_ms,workers,device_ms,sqp_iteration_rate_hz,solve_iterations_per_s,pcg_its_mean"]
+    header = "M,N,median_ms,p90_ms,workers,device_ms,sqp_iteration_rate_hz,solve_iterations_per_s,pcg_its_mean"
+    if args.cpu:
+        header += ",cpu_port_ms_est,cpu_cores,speedup_vs_cpu_port"
+    rows = [header]
+    cpu_wave = {}
     M_list = [m for m in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512) if m <= args.max_batch]
     for N in (16, 32, 64, 128):
         h = 0.05 if N >= 64 else 0.02
@@ -45,8 +53,22 @@ def main():
             med = wall[len(wall) // 2]
             p90 = wall[min(len(wall) - 1, int(np.ceil(0.9 * len(wall))) - 1)]
             d = float(np.median(dev))
-            rows.append(f"{M},{N},{med:.4f},{p90:.4f},gpu,{d:.4f},{args.iters * 1e3 / d:.1f},"
-                        f"{M * args.iters * 1e3 / d:.1f},{res.trace[:, :args.iters, 4].mean():.1f}")
+            row = (f"{M},{N},{med:.4f},{p90:.4f},gpu,{d:.4f},{args.iters * 1e3 / d:.1f},"
+                   f"{M * args.iters * 1e3 / d:.1f},{res.trace[:, :args.iters, 4].mean():.1f}")
+            if args.cpu:
+                import math
+                import os
+                import bench
+                cores = os.cpu_count() or 1
+                count = min(M, cores)
+                if (N, count) not in cpu_wave:
+                    w = dict(M=count, N=N, h=h, kind="reach", sqp=args.iters)
+                    wave_batch = workloads.iiwa14_reach_arrays(count, N)
+                    bench.cpu_step(w, wave_batch, count, cores)              # warm-up (imports, pool)
+                    cpu_wave[(N, count)] = 1e3 * bench.cpu_step(w, wave_batch, count, cores)
+                cpu_ms = cpu_wave[(N, count)] * math.ceil(M / cores)
+                row += f",{cpu_ms:.1f},{cores},{cpu_ms / med:.0f}"
+            rows.append(row)
             print(rows[-1], flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text("\n".join(rows) + "\n")
