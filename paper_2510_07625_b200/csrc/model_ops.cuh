@@ -51,7 +51,7 @@ cudaError_t launch_linearize(const RowView& V, const ModelParams& mp, double h, 
     k_linearize_simple<Mdl><<<(unsigned)((rows + threads - 1) / threads), threads, 0, s>>>(V, mp, h, rows, A, B, e);
   } else {
     iiwa::Stage* stages = static_cast<iiwa::Stage*>(scratch);
-    k_lin_primal_iiwa<0><<<(unsigned)((rows + linp::KNOTS - 1) / linp::KNOTS), 96, 4 * sizeof(linp::Slot), s>>>(
+    k_lin_primal_iiwa<0><<<(unsigned)((rows + linp::KNOTS - 1) / linp::KNOTS), 96, linp::smem_bytes(), s>>>(
         V, h, rows, stages, e);
     {
       static int minb = 0;
@@ -179,7 +179,7 @@ cudaError_t prepare_attrs(const SolveParams& P) {
   cudaError_t err;
   if constexpr (!Mdl::ANALYTIC_JAC) {
     err = cudaFuncSetAttribute(k_lin_primal_iiwa<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(4 * sizeof(linp::Slot)));
+                               (int)linp::smem_bytes());
     if (err != cudaSuccess) return err;
   }
   err = cudaFuncSetAttribute(k_schur<NX, NU, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,

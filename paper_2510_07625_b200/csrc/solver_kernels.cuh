@@ -374,12 +374,14 @@ __global__ void k_linearize_simple(RowView V, ModelParams mp, double h, int64_t 
 // barrier is ever reused.
 namespace linp {
 constexpr int KNOTS = 32;
+constexpr size_t smem_bytes();
 struct Slot {             // one RK4 stage of one CTA
   double L[28][KNOTS];
   double invd[7][KNOTS];
   double qdd[7][KNOTS];
   double xnext[14][KNOTS];   // stage point of the NEXT stage
 };
+constexpr size_t smem_bytes() { return 4 * sizeof(Slot) + KNOTS * sizeof(iiwa::Stage); }
 __device__ __forceinline__ void bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -394,6 +396,7 @@ __global__ void __launch_bounds__(96) k_lin_primal_iiwa(RowView V, double h, int
   constexpr int NX = 14, NU = 7, NF = 3, NJ = 7;
   extern __shared__ __align__(16) unsigned char linp_smem[];
   linp::Slot* slots = reinterpret_cast<linp::Slot*>(linp_smem);
+  iiwa::Stage* rec = reinterpret_cast<iiwa::Stage*>(slots + 4);   // [KNOTS] staging of the stage records
   const int role = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * linp::KNOTS + lane;
   bool valid = r < rows;
@@ -488,12 +491,6 @@ __global__ void __launch_bounds__(96) k_lin_primal_iiwa(RowView V, double h, int
       for (int i = 0; i < NJ; ++i) sl.invd[i][lane] = invd[i];
       __threadfence_block();
       linp::bar_sync(1 + s, 64);
-      if (valid) {
-#pragma unroll
-        for (int i = 0; i < 28; ++i) st[s].L[i] = L[i];
-#pragma unroll
-        for (int i = 0; i < NJ; ++i) st[s].invd[i] = invd[i];
-      }
     }
     linp::bar_sync(5 + 3, 96);
   } else {
@@ -508,20 +505,33 @@ __global__ void __launch_bounds__(96) k_lin_primal_iiwa(RowView V, double h, int
       linp::bar_sync(5 + s, 96);
 #pragma unroll
       for (int i = 0; i < NJ; ++i) qdd[i] = slots[s].qdd[i][lane];
-      // invalid lanes write their (dummy) record to a scratch copy of knot 0's slot: harmless only if
-      // nobody reads it, so give them a private dump instead
+      // The stage record (182 doubles) is assembled in this lane's shared-memory slot and leaves with
+      // ONE bulk async store (TMA) per knot and stage: 1456 contiguous bytes instead of 182 scattered
+      // 8-byte stores per lane.  The slot is reused once the previous store has read it.
+      if (s > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       if (valid) {
+        iiwa::Stage* mine = rec + lane;
 #pragma unroll
         for (int i = 0; i < NJ; ++i) {
-          st[s].s[i] = sn[i];
-          st[s].c[i] = cs[i];
-          st[s].qd[i] = xs[NJ + i];
+          mine->s[i] = sn[i];
+          mine->c[i] = cs[i];
+          mine->qd[i] = xs[NJ + i];
         }
-        iiwa::newton_euler<true, false>(sn, cs, xs + NJ, qdd, fw, tau, st + s);
+        iiwa::newton_euler<true, false>(sn, cs, xs + NJ, qdd, fw, tau, mine);
+#pragma unroll
+        for (int i = 0; i < 28; ++i) mine->L[i] = slots[s].L[i][lane];
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) mine->invd[i] = slots[s].invd[i][lane];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(st + s),
+                     "r"((unsigned)__cvta_generic_to_shared(mine)), "r"((unsigned)sizeof(iiwa::Stage))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
 #pragma unroll
       for (int i = 0; i < NX; ++i) xs[i] = slots[s].xnext[i][lane];
     }
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // shared memory must outlive the reads
   }
 }
 
