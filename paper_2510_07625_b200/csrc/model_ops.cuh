@@ -187,7 +187,6 @@ cudaError_t prepare_attrs(const SolveParams& P) {
   if (err != cudaSuccess) return err;
   {
     const PcgShape sh = pcg_shape<Mdl>(P.N, P.M);
-    if (!sh.smem && sh.bytes > 48 * 1024) return cudaErrorInvalidConfiguration;
     err = pcg_dispatch<Mdl>(sh, [&](auto kernel) {
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.bytes);
       if (e == cudaSuccess && sh.minb == 2)
