@@ -11,6 +11,7 @@
  *   gato_pcg_batched                          replaces blocktri.pcg / btmv          blocktri.py:105-173
  *   gato_shift_warm_start                     replaces mpc.shift_warm_start         mpc.py:85-89
  *   gato_best_of_batch                        replaces the best-of-batch argmin     mpc.py:283-298
+ *   gato_select_hypothesis                    replaces mpc.select_hypothesis        mpc.py:130-147
  *   gato_solve_host                           one control step of _MpcEngine.advance mpc.py:240-274
  *
  * The reference is pure Python and has no FFI of its own; INTEGRATION.md shows the ctypes
@@ -178,6 +179,15 @@ void gato_destroy(gato_handle* h);
 /* out[r] = one RK4 step of model from (X[r], U[r]) under force F[r], rows independent. */
 int gato_step_many(int32_t model_id, const double* model_params, int64_t rows, const double* X,
                    const double* U, const double* F, double timestep, double* out, void* stream);
+/* Hypothesis selection (mpc.py:130-147): every candidate force forces[j] (constant over the period)
+ * rolls the plant from x_prev with the applied control held for `substeps` RK4 steps of h_plant
+ * (simulate_plant, dynamics.py:843-864); *best = index of the candidate whose prediction is closest to
+ * x_meas in the 2-norm (positions only if position_only), first minimum on ties; errors[candidates]
+ * (optional) receives the distances. Device pointers, asynchronous. */
+int gato_select_hypothesis(int32_t model_id, const double* model_params, int32_t candidates,
+                           const double* x_prev, const double* u_applied, const double* x_meas,
+                           const double* forces, double h_plant, int32_t substeps, int32_t position_only,
+                           double* errors, int32_t* best, void* stream);
 /* A[r] (n x n), B[r] (n x m): exact Jacobians of the RK4 map at row r. */
 int gato_step_jacobians_many(int32_t model_id, const double* model_params, int64_t rows,
                              const double* X, const double* U, const double* F, double timestep,

@@ -7,7 +7,8 @@ kernels behind the C ABI in include/gato_b200.h.  There is no CPU execution path
 """
 
 from .batch import BatchSpec, batch_solve, bench_scaling, clear_engine_cache, shard_bounds, sqp_solve
-from .engine import BatchEngine, PackedBatch, PackedResult, pcg_batched, step_jacobians_many, step_many
+from .engine import (BatchEngine, PackedBatch, PackedResult, pcg_batched, select_hypothesis, step_jacobians_many,
+                     step_many)
 from .errors import (BackendUnavailableError, ConfigError, DimensionError, FactorizationError,
                      PcgBreakdownError)
 from .models import Cartpole, DoubleIntegrator, DynamicsModel, Iiwa14, Pendulum, TwoLinkArm
@@ -23,5 +24,5 @@ __all__ = [
     "FactorizationError", "Iiwa14", "IterationRecord", "LineSearchSettings", "PackedBatch",
     "PackedResult", "PcgBreakdownError", "PcgSettings", "Pendulum", "ProblemSpec", "SolverSettings",
     "SqpResult", "TwoLinkArm", "batch_solve", "bench_scaling", "clear_engine_cache", "pcg_batched", "shard_bounds",
-    "sqp_solve", "step_jacobians_many", "step_many",
+    "select_hypothesis", "sqp_solve", "step_jacobians_many", "step_many",
 ]

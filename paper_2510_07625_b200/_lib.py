@@ -62,6 +62,9 @@ EXPORTS = {
     "gato_destroy": (None, [C.c_void_p]),
     "gato_step_many": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int64, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
+    "gato_select_hypothesis": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int32, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p,
+                                         C.c_void_p, C.c_void_p]),
     "gato_step_jacobians_many": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int64, C.c_void_p,
                                            C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                            C.c_void_p, C.c_void_p]),

@@ -585,6 +585,21 @@ int gato_step_many(int32_t model_id, const double* model_params, int64_t rows, c
   return err == cudaSuccess ? GATO_OK : GATO_E_CUDA;
 }
 
+int gato_select_hypothesis(int32_t model_id, const double* model_params, int32_t candidates, const double* x_prev,
+                           const double* u_applied, const double* x_meas, const double* forces, double h_plant,
+                           int32_t substeps, int32_t position_only, double* errors, int32_t* best, void* stream) {
+  ModelOps ops;
+  if (!select_ops(model_id, model_params, &ops) || candidates < 1 || substeps < 1 || !(h_plant > 0.0) || !x_prev ||
+      !u_applied || !x_meas || !forces || !best)
+    return GATO_E_INVALID;
+  ModelParams mp;
+  for (int i = 0; i < 8; ++i) mp.v[i] = model_params ? model_params[i] : 0.0;
+  const int ncmp = position_only ? ops.nx / 2 : ops.nx;   // state layout [positions, velocities] (dynamics.py:9)
+  cudaError_t err = ops.select_hypothesis(mp, candidates, x_prev, u_applied, x_meas, forces, h_plant, substeps, ncmp,
+                                          errors, best, static_cast<cudaStream_t>(stream));
+  return err == cudaSuccess ? GATO_OK : GATO_E_CUDA;
+}
+
 int gato_step_jacobians_many(int32_t model_id, const double* model_params, int64_t rows, const double* X,
                              const double* U, const double* F, double timestep, double* A, double* B,
                              void* stream) {

@@ -22,6 +22,8 @@ struct ModelOps {
   cudaError_t (*linesearch)(const SolveParams&, cudaStream_t);
   cudaError_t (*step_rows)(const ModelParams&, double, int64_t, const double*, const double*, const double*,
                            double*, cudaStream_t);
+  cudaError_t (*select_hypothesis)(const ModelParams&, int, const double*, const double*, const double*,
+                                   const double*, double, int, int, double*, int32_t*, cudaStream_t);
   size_t (*pcg_mat_doubles)(int N);            // per-solve padded matrix record (PcgLayout)
   cudaError_t (*prepare)(const SolveParams&);  // opt-in shared memory sizes, outside any capture
 };
@@ -169,6 +171,15 @@ cudaError_t launch_step_rows(const ModelParams& mp, double h, int64_t rows, cons
 }
 
 template <class Mdl>
+cudaError_t launch_select_hypothesis(const ModelParams& mp, int M, const double* x_prev, const double* u_applied,
+                                     const double* x_meas, const double* forces, double h_plant, int substeps,
+                                     int ncmp, double* errors, int32_t* best, cudaStream_t s) {
+  k_select_hypothesis<Mdl><<<1, 256, 0, s>>>(mp, M, x_prev, u_applied, x_meas, forces, h_plant, substeps, ncmp,
+                                             errors, best);
+  return cudaGetLastError();
+}
+
+template <class Mdl>
 size_t pcg_mat_doubles(int N) {
   return PcgLayout<Mdl::NX>::mat_doubles(N);
 }
@@ -209,7 +220,8 @@ template <class Mdl>
 ModelOps make_ops() {
   return ModelOps{Mdl::NX,           Mdl::NU,           Mdl::NF,
                   launch_hessinv<Mdl>, launch_linearize<Mdl>, lin_scratch_bytes<Mdl>, launch_schur<Mdl>,
-                  launch_pcg<Mdl>,     launch_linesearch<Mdl>, launch_step_rows<Mdl>, pcg_mat_doubles<Mdl>, prepare_attrs<Mdl>};
+                  launch_pcg<Mdl>,     launch_linesearch<Mdl>, launch_step_rows<Mdl>, launch_select_hypothesis<Mdl>,
+                  pcg_mat_doubles<Mdl>, prepare_attrs<Mdl>};
 }
 
 

@@ -617,6 +617,75 @@ __global__ void k_step_rows(ModelParams mp, double h, int64_t rows, const double
   for (int i = 0; i < NX; ++i) out[r * NX + i] = o[i];
 }
 
+// k_select_hypothesis (mpc.py:130-147 with simulate_plant, dynamics.py:843-864): candidate j rolls the
+// plant from x_prev over one control period -- `substeps` RK4 steps of h_plant with the applied control
+// held and its own constant force -- and scores ||(pred - x_meas)[:ncmp]||_2; the first minimum wins
+// (np.argmin: the first NaN if there is one).  One CTA, one thread per candidate.
+template <class Mdl>
+__global__ void __launch_bounds__(256) k_select_hypothesis(ModelParams mp, int M, const double* __restrict__ x_prev,
+                                                           const double* __restrict__ u_applied,
+                                                           const double* __restrict__ x_meas,
+                                                           const double* __restrict__ forces, double h_plant,
+                                                           int substeps, int ncmp, double* __restrict__ errors,
+                                                           int32_t* __restrict__ best) {
+  constexpr int NX = Mdl::NX, NU = Mdl::NU, NF = Mdl::NF;
+  __shared__ double s_e[256];
+  __shared__ int s_i[256];
+  double be = INFINITY;
+  int bi = INT_MAX;
+  bool bnan = false;
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    double x[NX], u[NU], f[NF], o[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) x[i] = x_prev[i];
+#pragma unroll
+    for (int i = 0; i < NU; ++i) u[i] = u_applied[i];
+#pragma unroll
+    for (int i = 0; i < NF; ++i) f[i] = forces[(size_t)j * NF + i];
+    for (int sstep = 0; sstep < substeps; ++sstep) {
+      rk4_step<Mdl>(mp, x, u, f, h_plant, o);
+#pragma unroll
+      for (int i = 0; i < NX; ++i) x[i] = o[i];
+    }
+    double e2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      const double d = x[i] - x_meas[i];
+      if (i < ncmp) e2 = fma(d, d, e2);
+    }
+    const double e = sqrt(e2);
+    if (errors) errors[j] = e;
+    const bool isn = e != e;
+    // ascending j within a thread: keep the first NaN, else the first minimum
+    if (!bnan && (isn || bi == INT_MAX || e < be)) {
+      be = e;
+      bi = j;
+      bnan = isn;
+    }
+  }
+  s_e[threadIdx.x] = be;
+  s_i[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double e1 = s_e[threadIdx.x], e2 = s_e[threadIdx.x + o];
+      const int i1 = s_i[threadIdx.x], i2 = s_i[threadIdx.x + o];
+      const bool n1 = e1 != e1, n2 = e2 != e2;
+      bool take;
+      if (i2 == INT_MAX) take = false;
+      else if (i1 == INT_MAX) take = true;
+      else if (n1 || n2) take = n2 && (!n1 || i2 < i1);
+      else take = e2 < e1 || (e2 == e1 && i2 < i1);
+      if (take) {
+        s_e[threadIdx.x] = e2;
+        s_i[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && best) *best = s_i[0] == INT_MAX ? -1 : s_i[0];
+}
+
 // smallest even m >= n with m / 2 odd: a block stride of m doubles puts consecutive lanes on
 // distinct 16-byte bank groups for 128-bit shared-memory loads
 __host__ __device__ constexpr int pad_stride(int n) {

@@ -368,6 +368,39 @@ def step_many(model, X, U, h: float, F) -> np.ndarray:
     return out.cpu().numpy()
 
 
+def select_hypothesis(model, x_prev, u_applied, x_meas, forces, control_period: float, h_plant: float = 0.001,
+                      position_only: bool = False, return_errors: bool = False):
+    """Index of the candidate force whose one-period plant prediction best matches the measurement
+    (mpc.select_hypothesis, mpc.py:130-147; plant = fixed-substep RK4, dynamics.py:820-864), computed on
+    the GPU by gato_select_hypothesis.  ``forces``: (M, force_dim) constant candidates (a
+    ``HypothesisSet.forces`` array); ties break toward the lowest index."""
+    torch = _torch()
+    lib = _lib.load()
+    model_id, params = device_model(model)
+    ratio = control_period / h_plant
+    substeps = round(ratio)
+    if h_plant <= 0 or substeps < 1 or abs(ratio - substeps) > 1e-9 * max(1.0, abs(ratio)):
+        raise ValueError(f"control period {control_period} is not an integer multiple of plant substep {h_plant}")
+    forces = np.ascontiguousarray(forces, dtype=float)
+    if forces.ndim != 2 or forces.shape[1] != model.force_dim:
+        raise ValueError(f"forces must have shape (M, {model.force_dim})")
+    xs = [np.ascontiguousarray(v, dtype=float).reshape(-1) for v in (x_prev, u_applied, x_meas)]
+    if xs[0].size != model.state_dim or xs[1].size != model.control_dim or xs[2].size != model.state_dim:
+        raise ValueError("x_prev, u_applied, x_meas do not match the model dimensions")
+    dxp, du, dxm, df = (_dev(torch, v) for v in (*xs, forces))
+    M = forces.shape[0]
+    err = torch.empty(M, dtype=torch.float64, device="cuda")
+    best = torch.empty(1, dtype=torch.int32, device="cuda")
+    p = (C.c_double * 8)(*params)
+    rc = lib.gato_select_hypothesis(model_id, p, M, dxp.data_ptr(), du.data_ptr(), dxm.data_ptr(), df.data_ptr(),
+                                    float(h_plant), int(substeps), 1 if position_only else 0, err.data_ptr(),
+                                    best.data_ptr(), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"gato_select_hypothesis failed ({rc})")
+    idx = int(best.item())
+    return (idx, err.cpu().numpy()) if return_errors else idx
+
+
 def step_jacobians_many(model, X, U, h: float, F):
     """Row-wise exact RK4 Jacobians on the GPU (dynamics.py:774-802)."""
     torch = _torch()

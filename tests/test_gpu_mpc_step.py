@@ -104,3 +104,34 @@ def test_bench_scaling_rows_follow_the_reference_schema():
         gb.bench_scaling(gb.ProblemSpec(model=gb.Pendulum(), cost=gb.CostSpec(
             Q=np.eye(2), R=0.1 * np.eye(1), QN=np.eye(2), goal=np.zeros((9, 2))), horizon=8, timestep=0.05,
             x_start=np.zeros(2)), [1], [8])
+
+
+@pytest.mark.parametrize("model_name", ["two_link_arm", "iiwa14", "pendulum"])
+@pytest.mark.parametrize("position_only", [False, True])
+def test_select_hypothesis_matches_the_plant_rollout(model_name, position_only):
+    """mpc.select_hypothesis (mpc.py:130-147): every candidate force rolls the plant over one control
+    period in RK4 substeps (dynamics.py:843-864); distances and the chosen index against the oracle's
+    row-wise RK4 applied substep by substep."""
+    from oracle import trajopt_np as orc
+    rng = np.random.default_rng(31)
+    model = {"two_link_arm": gb.TwoLinkArm(), "iiwa14": gb.Iiwa14(), "pendulum": gb.Pendulum()}[model_name]
+    omodel = orc.model_from_descriptor(model)
+    n, m, fd = model.state_dim, model.control_dim, model.force_dim
+    M, period, h_plant = 37, 0.01, 0.001
+    x_prev = 0.3 * rng.standard_normal(n)
+    u = 0.5 * rng.standard_normal(m)
+    forces = np.stack([c.value for c in mpc.sample_hypotheses(np.zeros(fd), 2.0, M, seed=5)])
+    truth = 11                                    # the measurement comes from candidate 11's force
+    X = np.tile(x_prev, (M, 1))
+    for _ in range(10):
+        X = orc.rk4_rows(omodel, X, np.tile(u, (M, 1)), h_plant, forces)
+    x_meas = X[truth] + 1e-9 * rng.standard_normal(n)
+    sel = slice(0, n // 2) if position_only else slice(None)
+    want = np.linalg.norm((X - x_meas)[:, sel], axis=1)
+    idx, err = gb.select_hypothesis(model, x_prev, u, x_meas, forces, period, h_plant, position_only,
+                                    return_errors=True)
+    # one-dimensional force channels only have the two candidates center -+ sigma: ties go to the first
+    assert idx == int(np.argmin(want)) and np.array_equal(forces[idx], forces[truth])
+    assert np.max(np.abs(err - want)) <= 1e-11 * max(1.0, want.max())
+    with pytest.raises(ValueError):
+        gb.select_hypothesis(model, x_prev, u, x_meas, forces, 0.0105, h_plant)
