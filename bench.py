@@ -209,6 +209,31 @@ def cpu_baseline(w, batch, budget_s):
             "seconds_per_sample": t}
 
 
+def cpu_baseline_c(w, batch, budget_s):
+    """Second CPU arm: the compiled C restatement of the same algorithm (oracle/trajopt_c.c, POSIX threads
+    over the solves) on all host cores, bounded sample.  Not the reference's own implementation (that is
+    the numpy arm above); reported so that the GPU/CPU ratio can also be read against compiled code."""
+    from oracle import trajopt_c as oc
+    from oracle import trajopt_np as orc
+    cores = os.cpu_count() or 1
+    st = orc.Settings(max_sqp_iterations=w["sqp"], pcg_tolerance=1e-6, pcg_max_iterations=200, step_tolerance=None)
+    count = min(batch.size, 8 * cores)
+
+    def once():
+        t0 = time.perf_counter()
+        oc.solve_batch(batch.x_start[:count], batch.goal[:count], batch.Q[:count], batch.R[:count], batch.QN[:count],
+                       batch.force[:count], batch.rho_init[:count], batch.X[:count], batch.U[:count], w["h"], st,
+                       threads=cores)
+        return time.perf_counter() - t0
+
+    t1 = once()
+    reps = max(1, min(5, int(budget_s / max(t1, 1e-3)) - 1))
+    t = statistics.median([once() for _ in range(reps)])
+    return {"value": count * w["sqp"] / t, "unit": UNIT, "cores": cores, "kind": "port-c",
+            "sample": f"{count} of the workload's solves x {w['sqp']} SQP iteration(s), {cores} POSIX threads, "
+                      f"median of {reps} run(s) after 1 warm-up", "seconds_per_sample": t}
+
+
 def run_reference_arm(args, w, rank, world):
     """bench.py --impl reference: the reference's CPU implementation of the path (numpy; here its
     bitwise-pinned oracle port, since /root/reference does not exist on the GPU box) timed on the
@@ -453,6 +478,8 @@ def run_gpu_arm(args, w, rank, local_rank, world):
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, batch, args.cpu_budget_s)
             line["e2e_speedup_vs_cpu_baseline"] = e2e_value / line["cpu_baseline"]["value"]
+            line["cpu_baseline_c"] = cpu_baseline_c(w, batch, min(args.cpu_budget_s, 10.0))
+            line["e2e_speedup_vs_cpu_baseline_c"] = e2e_value / line["cpu_baseline_c"]["value"]
         print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:

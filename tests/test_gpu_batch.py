@@ -189,3 +189,33 @@ def test_baseline_size_properties(M, N, h, kind):
             assert np.max(np.abs(full.trace[b, :, _lib.TRACE_PCG_ITERATIONS] - pcg_ref)) <= 1
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("M,N,h,kind", [(32, 32, 0.02, "track"), (128, 64, 0.05, "reach"), (256, 16, 0.02, "reach")])
+def test_every_solve_of_the_baseline_batches_matches_the_compiled_oracle(M, N, h, kind):
+    """BASELINE.json configs[1] and configs[2] at full size, EVERY solve: the compiled C restatement
+    (oracle/trajopt_c.c, itself checked against the bitwise-pinned numpy oracle in tests/test_oracle_c.py)
+    is fast enough to serve as the checker for whole batches.  Trajectories within 1e-6 relative (the
+    north-star bar is 1e-4), identical SQP iteration counts, PCG counts within +-1, identical step
+    lengths and accept decisions."""
+    from oracle import trajopt_c as oc
+    from oracle import trajopt_np as orc
+    batch = workloads.iiwa14_track_arrays(M, N, h) if kind == "track" else workloads.iiwa14_reach_arrays(M, N)
+    iters = 1 if kind == "track" else 5
+    st = workloads.fixed_budget_settings(iters)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, h, st)
+    try:
+        got = eng.solve(batch)
+    finally:
+        eng.close()
+    ost = orc.Settings(max_sqp_iterations=iters, pcg_tolerance=1e-6, pcg_max_iterations=200, step_tolerance=None)
+    X, U, trace, info = oc.solve_batch(batch.x_start, batch.goal, batch.Q, batch.R, batch.QN, batch.force,
+                                       batch.rho_init, batch.X, batch.U, h, ost)
+    assert np.all(info[:, 2] == 0) and np.all(got.info[:, _lib.INFO_STATUS] == 0)
+    assert np.array_equal(got.info[:, _lib.INFO_N_RECORDS], info[:, 0])
+    worst = max(max(rel_inf(got.X[b], X[b]), rel_inf(got.U[b], U[b])) for b in range(M))
+    assert worst <= 1e-6, f"worst trajectory error over {M} solves: {worst:.3e}"
+    assert np.max(np.abs(got.trace[:, :, _lib.TRACE_PCG_ITERATIONS] - trace[:, :, 4])) <= 1
+    assert np.array_equal(got.trace[:, :, _lib.TRACE_ALPHA], trace[:, :, 2])
+    assert np.array_equal(got.trace[:, :, _lib.TRACE_ACCEPTED], trace[:, :, 5])
+    assert rel_inf(got.trace[:, :, _lib.TRACE_MERIT], trace[:, :, 0]) <= 1e-8
