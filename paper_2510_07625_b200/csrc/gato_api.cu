@@ -67,7 +67,6 @@ struct gato_handle {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t launches = 0;
   void* lin_scratch = nullptr;  // model-private linearisation scratch (iiwa14: per-stage link data)
-  bool fuse_update = false;     // GATO_FUSE_UPDATE=1: update_solve as the tail of k_linesearch
 };
 
 namespace {
@@ -118,14 +117,6 @@ int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond, cudaEvent_t* mark
   if (marks) CK(cudaEventRecord(marks[3], s));
   CK(h->ops.pcg(P, s));
   if (marks) CK(cudaEventRecord(marks[4], s));
-  if (!marks && h->fuse_update) {   // the last line-search CTA of each solve applies the step
-    SolveParams Pl = P;
-    Pl.cond = (unsigned long long)h->cond;
-    Pl.use_cond = use_cond;
-    Pl.fuse_update = 1;
-    CK(h->ops.linesearch(Pl, s));
-    return GATO_OK;
-  }
   CK(h->ops.linesearch(P, s));
   if (marks) CK(cudaEventRecord(marks[5], s));
   k_update<<<P.M, 128, 0, s>>>(P, h->ops.nx, h->ops.nu, h->cond, use_cond);
@@ -278,7 +269,6 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   ALLOC(si, M * SI_WORDS);
   ALLOC(pcg_iters, M * P.max_it);
   ALLOC(counters, 8);
-  ALLOC(ls_ticket, M);
 #undef ALLOC
   if (rc != GATO_OK) return rc;
   {
@@ -301,9 +291,6 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CK(h->ops.prepare(P));
   h->loop_mode = cfg->loop_mode ? cfg->loop_mode : env_int("GATO_LOOP_MODE", 1);
-  // measured on B200 (M=32, N=32): 0.233 ms fused vs 0.229 ms with k_update as its own graph node -- the
-  // boundary costs less than the serial tail it adds to the last line-search CTA, so fusion is opt-in
-  h->fuse_update = env_int("GATO_FUSE_UPDATE", 0) != 0;
   return GATO_OK;
 }
 
@@ -478,9 +465,8 @@ int64_t gato_launch_count(const gato_handle* h) {
   if (!h) return 0;
   unsigned int c[4] = {0, 0, 0, 0};
   if (cudaMemcpy(c, h->P.counters, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  // k_init + per pass: k_hessinv, linearisation (two kernels for iiwa14), k_schur, PCG, k_linesearch
-  // (whose last CTA per solve applies the step) and k_update when it is not fused
-  const int per_pass = 4 + (h->ops.lin_scratch_bytes(1) > 0 ? 2 : 1) + (h->fuse_update ? 0 : 1);
+  // k_init + per pass: k_hessinv, linearisation (two kernels for iiwa14), k_schur, PCG, k_linesearch, k_update
+  const int per_pass = 5 + (h->ops.lin_scratch_bytes(1) > 0 ? 2 : 1);
   return 1 + per_pass * (int64_t)c[3];
 }
 

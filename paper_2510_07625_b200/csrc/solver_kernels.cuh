@@ -42,10 +42,6 @@ struct SolveParams {
   double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Linv, *Lfac, *pmats, *gamma, *gammaw, *lbw, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
   int32_t *si, *pcg_iters;
   unsigned int* counters;  // [0] active count, [1] ticket, [2] pending solves, [3] passes run
-  // fused tail of k_linesearch: its last CTA of a solve runs update_solve
-  unsigned int* ls_ticket;  // [M]
-  unsigned long long cond;  // cudaGraphConditionalHandle of the WHILE node
-  int use_cond, fuse_update;
 };
 
 // doubles per solve in hinv: [Qs^-1 | Qt^-1 | Rs^-1], padded to an even count (16-byte rows)
@@ -1038,7 +1034,7 @@ struct BlockReducer {
 };
 
 // -----------------------------------------------------------------------------------------
-// update_solve (one CTA per solve; k_update, or the last line-search CTA of the solve): first-minimum argmin over the candidates, strict-decrease accept test
+// update_solve (one CTA per solve, called by k_update): first-minimum argmin over the candidates, strict-decrease accept test
 // (sqp.py:193-195), X += a dX, U += a dU (sqp.py:277-281), IterationRecord (sqp.py:283-292),
 // adapt_rho (sqp.py:198-201), budget termination; counts the still-active solves and, when
 // run inside the WHILE graph node, sets its condition.
@@ -1151,19 +1147,16 @@ __global__ void __launch_bounds__(128, MINB) k_linesearch(SolveParams P) {
   const int c = blockIdx.x, b = blockIdx.y;
   const int32_t* si = P.si + b * SI_WORDS;
   const int skip = si[SI_SKIP_LS];
-  bool run;
   if (c < P.C) {
-    run = si[SI_ACTIVE] && !skip;
+    if (!si[SI_ACTIVE] || skip) return;
   } else {
     // candidate C is the current iterate (alpha = 0): merit(X0, U0) of sqp.py:229, needed once
-    run = (si[SI_ACTIVE] && !skip && !si[SI_MERIT_VALID]) || skip == 2;
+    if (!((si[SI_ACTIVE] && !skip && !si[SI_MERIT_VALID]) || skip == 2)) return;
   }
-  if (!run && !P.fuse_update) return;
   __shared__ double2 red[2 * 32];
-  __shared__ int bad_flag, is_last;
+  __shared__ int bad_flag;
   if (threadIdx.x == 0) bad_flag = 0;
   __syncthreads();
-  if (run) {
   const int N = P.N, nb = N + 1;
   const double alpha = (c < P.C) ? P.alphas[c] : 0.0;
   double cost = 0.0, viol = 0.0;
@@ -1239,21 +1232,6 @@ __global__ void __launch_bounds__(128, MINB) k_linesearch(SolveParams P) {
     if (bad_flag || !isfinite(value)) value = INFINITY;
     P.merits[(size_t)b * (P.C + 1) + c] = value;
     P.viols[(size_t)b * (P.C + 1) + c] = s.y;
-  }
-  }  // run
-  if (!P.fuse_update) return;
-  // the last CTA of this solve to get here applies the step (every candidate CTA takes a ticket,
-  // whether it evaluated a candidate or not)
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned ticket = atomicAdd(&P.ls_ticket[b], 1u);
-    is_last = ticket == gridDim.x - 1;
-    if (is_last) P.ls_ticket[b] = 0;
-  }
-  __syncthreads();
-  if (is_last) {
-    __threadfence();
-    update_solve(P, b, NX, NU, (cudaGraphConditionalHandle)P.cond, P.use_cond, gridDim.y);
   }
 }
 

@@ -191,9 +191,10 @@ def test_baseline_size_properties(M, N, h, kind):
         eng.close()
 
 
-@pytest.mark.parametrize("M,N,h,kind", [(32, 32, 0.02, "track"), (128, 64, 0.05, "reach"), (256, 16, 0.02, "reach")])
+@pytest.mark.parametrize("M,N,h,kind", [(32, 32, 0.02, "track"), (128, 64, 0.05, "reach"), (256, 16, 0.02, "reach"),
+                                          (1024, 64, 0.05, "reach")])
 def test_every_solve_of_the_baseline_batches_matches_the_compiled_oracle(M, N, h, kind):
-    """BASELINE.json configs[1] and configs[2] at full size, EVERY solve: the compiled C restatement
+    """BASELINE.json configs[1], configs[2] and the per-GPU shard of configs[4] at full size, EVERY solve: the compiled C restatement
     (oracle/trajopt_c.c, itself checked against the bitwise-pinned numpy oracle in tests/test_oracle_c.py)
     is fast enough to serve as the checker for whole batches.  Trajectories within 1e-6 relative (the
     north-star bar is 1e-4), identical SQP iteration counts, PCG counts within +-1, identical step
