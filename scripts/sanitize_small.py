@@ -1,7 +1,10 @@
 """Small solves of every kernel variant, for compute-sanitizer (memcheck / racecheck / synccheck).
     compute-sanitizer --tool racecheck python scripts/sanitize_small.py"""
+import os
 import sys
 from pathlib import Path
+
+os.environ.setdefault("GATO_LOOP_MODE", "3")   # plain stream launches: racecheck cannot follow conditional graph nodes
 
 import numpy as np
 
@@ -13,13 +16,16 @@ import paper_2510_07625_b200 as gb  # noqa: E402
 from paper_2510_07625_b200 import workloads  # noqa: E402
 from conftest import load_golden, product_problem, product_settings  # noqa: E402
 
-# iiwa14: real-time PCG (N=8), fat-thread PCG T=1 (N=40 > 35), global-memory PCG (N=70)
-for N, iters in ((8, 2), (40, 1), (70, 1)):
+# iiwa14: real-time PCG (N=8), fat-thread PCG with O^ and L resident (N=40 > 35), O^ resident only
+# (N=100), everything in global memory (N=150); the control-step call, best-of-batch, hypothesis selection
+for N, iters in ((8, 2), (40, 1), (100, 1), (150, 1)):
     batch = workloads.iiwa14_reach_arrays(3, N)
     eng = gb.BatchEngine(gb.Iiwa14(), 3, N, 0.02, workloads.fixed_budget_settings(iters), loop_mode=3)
     res = eng.solve(batch)
     eng.shift_warm_start()
     eng.stream.synchronize()
+    eng.step(batch, shift=True)
+    eng.best_of_batch()
     print("iiwa14 N", N, "status", res.info[:, 2].tolist(), "pcg", res.trace[:, 0, 4].tolist())
     eng.close()
 # the reference's analytic models (k_linearize_simple, small block sizes)
@@ -32,6 +38,7 @@ rng = np.random.default_rng(0)
 X, U, F = rng.standard_normal((5, 14)), rng.standard_normal((5, 7)), rng.standard_normal((5, 3))
 gb.step_many(gb.Iiwa14(), X, U, 0.02, F)
 gb.step_jacobians_many(gb.Iiwa14(), X, U, 0.02, F)
+gb.select_hypothesis(gb.Iiwa14(), X[0], U[0], X[1], F, 0.004, 0.001)
 d = np.tile(np.eye(3) * 4.0, (2, 5, 1, 1))
 o = 0.1 * rng.standard_normal((2, 4, 3, 3))
 gb.pcg_batched(d, o, rng.standard_normal((2, 15)), np.tile(np.eye(3) / 4.0, (2, 5, 1, 1)), np.zeros((2, 4, 3, 3)), 1e-10)
