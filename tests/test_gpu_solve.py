@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import paper_2510_07625_b200 as gb
-from paper_2510_07625_b200 import workloads
+from paper_2510_07625_b200 import _lib, workloads
 from paper_2510_07625_b200.batch import pack_problems
 from conftest import (ALL_CASES, load_golden, oracle_problem, oracle_settings, product_problem,
                       product_settings, rel_inf, trace_rows)
@@ -231,3 +231,26 @@ def test_random_instances_over_the_model_pool_match_the_oracle(seed):
         assert len(res.trace) == len(ref.trace) and res.converged == ref.converged
     upto = min(len(want), len(got), flip + 1)
     assert np.max(np.abs(got[:upto, 5] - want[:upto, 5])) <= 1
+
+
+@pytest.mark.parametrize("M,N", [(1, 1), (3, 2), (5, 3), (7, 35), (2, 36), (1, 255), (33, 5)])
+def test_boundary_horizons_match_the_compiled_oracle(M, N):
+    """Shortest horizons, the last horizon of the register-resident PCG kernel (N=35), the first of the
+    fat-thread kernel (N=36) and the longest supported one (N+1 = 256 block rows), iiwa14, against the
+    compiled C oracle: trajectories and per-iteration PCG counts."""
+    from oracle import trajopt_c as oc
+    from oracle import trajopt_np as orc
+    h = 0.02
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, h, workloads.fixed_budget_settings(2))
+    try:
+        got = eng.solve(batch)
+    finally:
+        eng.close()
+    ost = orc.Settings(max_sqp_iterations=2, pcg_tolerance=1e-6, pcg_max_iterations=200, step_tolerance=None)
+    X, U, trace, info = oc.solve_batch(batch.x_start, batch.goal, batch.Q, batch.R, batch.QN, batch.force,
+                                       batch.rho_init, batch.X, batch.U, h, ost)
+    assert np.all(got.info[:, _lib.INFO_STATUS] == 0) and np.all(info[:, 2] == 0)
+    assert rel_inf(got.X, X) <= 1e-6 and rel_inf(got.U, U) <= 1e-6
+    assert np.max(np.abs(got.trace[:, :, _lib.TRACE_PCG_ITERATIONS] - trace[:, :, 4])) <= 1
+    assert np.array_equal(got.trace[:, :, _lib.TRACE_ALPHA], trace[:, :, 2])
