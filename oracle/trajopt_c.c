@@ -293,7 +293,7 @@ static int cholesky(double* A, int d) {
   for (int j = 0; j < d; ++j) {
     double s = A[j * d + j];
     for (int k = 0; k < j; ++k) s -= A[j * d + k] * A[j * d + k];
-    if (!(s > 0.0)) return j + 1;
+    if (s <= 0.0) return j + 1; /* NaN passes, as in scipy's cho_factor over OpenBLAS */
     const double r = sqrt(s);
     A[j * d + j] = r;
     for (int i = j + 1; i < d; ++i) {

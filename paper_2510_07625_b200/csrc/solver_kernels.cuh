@@ -53,7 +53,7 @@ __device__ __forceinline__ int tri_idx(int i, int j) { return i >= j ? i * (i + 
 
 // -----------------------------------------------------------------------------------------
 // Warp-cooperative SPD inverse: lower Cholesky, solve against I, symmetrise
-// (qpform.py:261-268; failure semantics of LAPACK dpotrf: pivot <= 0 or NaN -> 1-based index).
+// (qpform.py:261-268; failure = pivot <= 0 -> 1-based index; NaN pivots pass, see warp_cholesky).
 // W: D*D row-major in shared memory (in: matrix, out: inverse), T: D*D scratch.
 // -----------------------------------------------------------------------------------------
 template <int D>
@@ -64,7 +64,10 @@ struct SpdScratch {
 };
 
 // lower Cholesky factor of the D*D matrix in W -> S.L (row stride D + 1, lower triangle), S.invd;
-// returns 0 or the 1-based index of the failing pivot (dpotrf semantics: pivot <= 0 or NaN).
+// returns 0 or the 1-based index of the failing pivot (pivot <= 0).  A NaN pivot passes, as it does in
+// the reference's scipy.linalg.cho_factor over OpenBLAS (whose potrf, unlike netlib's, has no DISNAN
+// test): with non-finite inputs the reference does not raise, it runs PCG to the cap on NaNs, scores
+// every candidate +inf and rejects the step (sqp.py:118-129, blocktri.py:158) -- and so does this path.
 // Right-looking, the lower triangle lives in REGISTERS spread over the 32 lanes (entry p = lane + 32 e
 // of the packed triangle): per pivot one shuffle broadcasts the diagonal, every lane forms sqrt and
 // rsqrt itself, the owners publish the scaled column through shared memory (one __syncwarp) and each
@@ -90,7 +93,7 @@ __device__ __forceinline__ int warp_cholesky(const double* W, SpdScratch<D>& S, 
   for (int j = 0; j < D; ++j) {
     const int pj = j * (j + 1) / 2 + j;
     const double d = __shfl_sync(0xffffffffu, a[pj >> 5], pj & 31);
-    if (!(d > 0.0)) {
+    if (d <= 0.0) {   // a NaN pivot is NOT a failure: see the note above
       fail = j + 1;
       break;
     }

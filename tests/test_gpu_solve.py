@@ -254,3 +254,27 @@ def test_boundary_horizons_match_the_compiled_oracle(M, N):
     assert rel_inf(got.X, X) <= 1e-6 and rel_inf(got.U, U) <= 1e-6
     assert np.max(np.abs(got.trace[:, :, _lib.TRACE_PCG_ITERATIONS] - trace[:, :, 4])) <= 1
     assert np.array_equal(got.trace[:, :, _lib.TRACE_ALPHA], trace[:, :, 2])
+
+
+def test_non_finite_initial_guess_behaves_like_the_reference():
+    """A NaN in the initial trajectory does not raise in the reference (scipy's Cholesky over OpenBLAS lets
+    NaN pivots through): every SQP iteration runs PCG to its cap on NaNs, all candidates score +inf, the
+    step is rejected, rho grows and the iterate is returned untouched.  Same records from the device."""
+    from oracle import trajopt_np as orc
+    problem = gb.ProblemSpec(model=gb.Pendulum(),
+                             cost=gb.CostSpec(Q=np.diag([1.0, 0.1]), R=np.diag([0.01]), QN=np.diag([100.0, 10.0]),
+                                              goal=np.array([np.pi, 0.0])),
+                             horizon=8, timestep=0.05, x_start=np.zeros(2))
+    X = np.zeros((9, 2))
+    X[3, 0] = np.nan
+    U = np.zeros((8, 1))
+    st = gb.SolverSettings(max_sqp_iterations=3, step_tolerance=None)
+    res = gb.sqp_solve(problem, X, U, st)
+    ref = orc.solve(orc.Problem.from_spec(problem), X, U, orc.Settings(max_sqp_iterations=3, step_tolerance=None))
+    assert len(res.trace) == len(ref.trace) == 3 and not res.converged
+    for got, want in zip(res.trace, ref.trace):
+        assert got.merit == want.merit == np.inf and got.alpha == want.alpha == 1.0
+        assert got.accepted is False and want.accepted is False
+        assert got.pcg_iterations == want.pcg_iterations == 10 * 9 * 2
+        assert got.rho == want.rho and np.isnan(got.step_inf_norm) and np.isnan(want.step_inf_norm)
+    assert np.array_equal(res.X, X, equal_nan=True) and np.array_equal(res.U, U)
