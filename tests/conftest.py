@@ -16,7 +16,9 @@ REFERENCE_SRC = Path("/root/reference/pkg/src")
 
 STAGED_CASES = ["pendulum_n8", "cartpole_n8", "twolink_n8", "twolink_gravity_n8", "di1_n4", "di2_n4",
                 "di7_n8", "pendulum_n8_tol", "twolink_n8_tol", "iiwa14_random_n8", "iiwa14_reach_n8_b0",
-                "iiwa14_reach_n8_b1", "iiwa14_track_n16_b0", "iiwa14_track_n16_b2"]
+                "iiwa14_reach_n8_b1", "iiwa14_track_n16_b0", "iiwa14_track_n16_b2",
+                # time-varying force + non-default line search + unregularised R; rho clamps; PCG cap reached
+                "twolink_profile_n8", "cartpole_rho_n8", "iiwa14_pcgcap_n16"]
 FINAL_ONLY_CASES = ["pendulum_swingup_n64", "iiwa14_reach_n32_c1", "iiwa14_reach_n16_tol"]
 ALL_CASES = STAGED_CASES + FINAL_ONLY_CASES
 
@@ -60,14 +62,26 @@ def product_settings(g):
         regularize_r=bool(s[12]), pcg_retry_limit=int(s[13]))
 
 
+class KnotTable:
+    """Force profile that returns the golden file's per-knot force at t = k*h."""
+
+    def __init__(self, table, h):
+        self.table, self.h = np.asarray(table, dtype=float), float(h)
+
+    def __call__(self, t):
+        return self.table[int(round(t / self.h))]
+
+
 def product_problem(g):
     import paper_2510_07625_b200 as gb
     model = product_model(g)
-    force = g["force"]
-    assert np.all(force == force[0])
+    force, h = g["force"], float(g["timestep"])
+    if np.all(force == force[0]):
+        ext = gb.ExternalForce.constant(force[0])
+    else:   # the reference sampled its profile at the knot start times k*h (qpform.py:113-123)
+        ext = gb.ExternalForce.time_varying(KnotTable(force, h), force.shape[1])
     return gb.ProblemSpec(model=model, cost=gb.CostSpec(g["Q"], g["R"], g["QN"], g["goal"]),
-                          horizon=int(g["horizon"]), timestep=float(g["timestep"]), x_start=g["x_start"],
-                          force=gb.ExternalForce.constant(force[0]))
+                          horizon=int(g["horizon"]), timestep=h, x_start=g["x_start"], force=ext)
 
 
 def oracle_settings(g):

@@ -17,6 +17,8 @@ import os
 import sys
 from pathlib import Path
 
+import dataclasses
+
 import numpy as np
 
 ROOT = Path(__file__).resolve().parents[2]
@@ -67,7 +69,12 @@ def trace_array(trace) -> np.ndarray:
                       float(r.accepted), r.step_inf_norm] for r in trace], dtype=float).reshape(-1, 8)
 
 
+ONLY = set(sys.argv[1:])      # python make_golden.py [case ...]: regenerate only the named cases
+
+
 def dump(name, problem, X0, U0, settings, stages=True):
+    if ONLY and name not in ONLY:
+        return
     N, n = problem.horizon, problem.model.state_dim
     goal = problem.cost.goal if problem.cost.goal.ndim == 2 else np.broadcast_to(problem.cost.goal, (N + 1, n))
     params = np.zeros(8)
@@ -157,6 +164,23 @@ def main():
     c1 = workloads.iiwa14_reach_arrays(1, 32)
     dump("iiwa14_reach_n32_c1", to_ref_problem(c1, 0, 0.02, iiwa), c1.X[0], c1.U[0],
          fixed(5, tol=1e-6, cap=200), stages=False)
+    # settings off the defaults, a time-varying force profile (dynamics.py:71-91), R not regularised
+    rng = np.random.default_rng(111)
+    arm = tb.TwoLinkArm(gravity=9.81)
+    prob, X, U = oracles.random_problem(rng, model=arm, N=8)
+    prob = dataclasses.replace(prob, force=tb.ExternalForce.time_varying(
+        tb.dynamics.SwingingLoadProfile(weight=1.5, amplitude=2.0, frequency_hz=2.0), 2))
+    dump("twolink_profile_n8", prob, X, U,
+         tb.SolverSettings(max_sqp_iterations=5, pcg=tb.PcgSettings(tolerance=1e-8), step_tolerance=None,
+                           regularize_r=False, line_search=tb.LineSearchSettings(mu=5.0, beta=3.0, num_shrinks=4)))
+    # rho clamped at both ends (sqp.py:198-201)
+    random_case("cartpole_rho_n8", 112, tb.Cartpole(), 8,
+                tb.SolverSettings(max_sqp_iterations=6, pcg=tb.PcgSettings(tolerance=1e-8), step_tolerance=None,
+                                  rho_init=1e-2, rho_factor=10.0, rho_min=1e-3, rho_max=1e-1))
+    # PCG stopped by its iteration cap (blocktri.py:78-81,173): the real-time budget regime
+    capped = workloads.iiwa14_reach_arrays(1, 16)
+    dump("iiwa14_pcgcap_n16", to_ref_problem(capped, 0, 0.02, iiwa), capped.X[0], capped.U[0],
+         fixed(3, tol=1e-6, cap=20))
     # tolerance mode on iiwa14
     t16 = workloads.iiwa14_reach_arrays(1, 16)
     dump("iiwa14_reach_n16_tol", to_ref_problem(t16, 0, 0.05, iiwa), t16.X[0], t16.U[0],
