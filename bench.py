@@ -478,8 +478,11 @@ def run_gpu_arm(args, w, rank, local_rank, world):
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, batch, args.cpu_budget_s)
             line["e2e_speedup_vs_cpu_baseline"] = e2e_value / line["cpu_baseline"]["value"]
-            line["cpu_baseline_c"] = cpu_baseline_c(w, batch, min(args.cpu_budget_s, 10.0))
-            line["e2e_speedup_vs_cpu_baseline_c"] = e2e_value / line["cpu_baseline_c"]["value"]
+            try:   # the compiled arm is an extra: never let it take the bench line down
+                line["cpu_baseline_c"] = cpu_baseline_c(w, batch, min(args.cpu_budget_s, 10.0))
+                line["e2e_speedup_vs_cpu_baseline_c"] = e2e_value / line["cpu_baseline_c"]["value"]
+            except Exception as exc:  # noqa: BLE001
+                line["cpu_baseline_c"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
         print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:
