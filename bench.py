@@ -313,9 +313,7 @@ def run_gpu_arm(args, w, rank, local_rank, world):
         state, warm start = device shift, goal window advanced); reach: solve from the cold init."""
         with torch.cuda.stream(stream):
             if track:
-                eng.dev["x_start"].copy_(eng.dev["X"][:, 1, :])
-                eng.shift_warm_start()
-                eng.dev["goal"].copy_(ref_dev[s:s + N + 1].unsqueeze(0).expand(M, N + 1, 14))
+                eng.mpc_advance(ref_dev, s)    # one kernel: measured state, device shift, goal window
             else:
                 eng.dev["X"].copy_(X0)
                 eng.dev["U"].copy_(U0)
@@ -347,7 +345,7 @@ def run_gpu_arm(args, w, rank, local_rank, world):
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     dev_ms = float(sum(step_ms))
-    launches_per_step = eng.launch_count() + (1 if track else 0)
+    launches_per_step = eng.launch_count() + (1 if track else 0)   # + k_mpc_advance
     res_last = eng.download()
     status_ok = bool(np.all(res_last.info[:, _lib.INFO_STATUS] == 0))
     pcg_last = res_last.trace[:, :K_sqp, _lib.TRACE_PCG_ITERATIONS]

@@ -12,7 +12,7 @@
  *   gato_shift_warm_start                     replaces mpc.shift_warm_start         mpc.py:85-89
  *   gato_best_of_batch                        replaces the best-of-batch argmin     mpc.py:283-298
  *   gato_select_hypothesis                    replaces mpc.select_hypothesis        mpc.py:130-147
- *   gato_solve_host                           one control step of _MpcEngine.advance mpc.py:240-274
+ *   gato_solve_host / gato_mpc_advance        one control step of _MpcEngine.advance mpc.py:240-274
  *
  * The reference is pure Python and has no FFI of its own; INTEGRATION.md shows the ctypes
  * stub a maintainer would add to trajbatch/batch.py to call this library.
@@ -137,6 +137,14 @@ int gato_bind(gato_handle* h, const gato_buffers* bufs);
 int gato_solve(gato_handle* h, void* stream);
 /* X <- [X[1:], X[-1]], U <- [U[1:], U[-1]] for every solve, in place (mpc.py:85-89). */
 int gato_shift_warm_start(gato_handle* h, void* stream);
+/* One control period of a device-resident MPC loop (mpc.py:240-274), in place on the bound buffers:
+ * x_start <- X[:, 1] (the predicted next state stands in for the measurement), X and U shifted one knot
+ * left with the tail duplicated (mpc.py:85-89), and -- if goal_path is given -- the goal window advanced
+ * to goal[k] = goal_path[min(step + k, path_len - 1)], k = 0..N. goal_path: device array [path_len, n]
+ * shared by all solves (path_stride = 0) or one path per solve (path_stride = path_len * n doubles).
+ * Writes the caller's x_start / goal / X / U buffers. Asynchronous. */
+int gato_mpc_advance(gato_handle* h, void* stream, const double* goal_path, int64_t path_len,
+                     int64_t path_stride, int64_t step);
 /* One control step with HOST buffers in a single call (the MPC caller's inner loop, mpc.py:240-274):
  * copy `in_bytes` from (pinned) host memory to `dev_in`, optionally shift the warm start, run the
  * solve to termination, copy `out_bytes` from `dev_out` back to host memory and synchronise the

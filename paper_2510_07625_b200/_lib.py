@@ -49,6 +49,7 @@ EXPORTS = {
     "gato_solve_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_int64]),
     "gato_best_of_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gato_mpc_advance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64]),
     "gato_pending": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
     "gato_resume": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "gato_loop_mode": (C.c_int, [C.c_void_p]),

@@ -45,6 +45,35 @@ __global__ void __launch_bounds__(128) k_update(SolveParams P, int nx, int nu, c
   update_solve(P, blockIdx.x, nx, nu, cond, use_cond, gridDim.x);
 }
 
+// One control period of the device-resident MPC loop (mpc.py:240-274), one CTA per solve, in place:
+//   x_start <- X[1]                         (the predicted next state stands in for the measurement)
+//   X, U    <- shifted one knot left, tail duplicated           (mpc.py:85-89)
+//   goal[k] <- path[min(step + k, path_len - 1)],  k = 0..N      (goal window advanced along the path)
+// path: [path_len, nx] shared by all solves (path_stride = 0) or one per solve (path_stride = path_len * nx).
+__global__ void k_mpc_advance(double* X, double* U, double* x_start, double* goal, const double* __restrict__ path,
+                              int64_t path_len, int64_t path_stride, int64_t step, int N, int nx, int nu) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.x;
+  double* Xb = X + (size_t)b * (N + 1) * nx;
+  double* Ub = U + (size_t)b * N * nu;
+  const int nX = (N + 1) * nx, nU = N * nu;
+  for (int i = threadIdx.x; i < nX; i += blockDim.x) sh[i] = Xb[i];
+  for (int i = threadIdx.x; i < nU; i += blockDim.x) sh[nX + i] = Ub[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) x_start[(size_t)b * nx + i] = sh[nx + i];
+  for (int i = threadIdx.x; i < nX; i += blockDim.x) Xb[i] = sh[(i + nx < nX) ? i + nx : i];
+  for (int i = threadIdx.x; i < nU; i += blockDim.x) Ub[i] = sh[nX + ((i + nu < nU) ? i + nu : i)];
+  if (path) {
+    const double* pb = path + (size_t)b * path_stride;
+    double* gb = goal + (size_t)b * nX;
+    for (int i = threadIdx.x; i < nX; i += blockDim.x) {
+      int64_t row = step + i / nx;
+      if (row > path_len - 1) row = path_len - 1;
+      gb[i] = pb[row * nx + i % nx];
+    }
+  }
+}
+
 // mpc.py:283-298: argmin of the final merit over the solves that did not fail, first minimum on ties.
 // One CTA; (merit, index) pairs compared lexicographically so the result does not depend on the
 // reduction order.

@@ -397,6 +397,26 @@ int gato_shift_warm_start(gato_handle* h, void* stream) {
   return GATO_OK;
 }
 
+int gato_mpc_advance(gato_handle* h, void* stream, const double* goal_path, int64_t path_len, int64_t path_stride,
+                     int64_t step) {
+  if (!h || !h->bound) return GATO_E_INVALID;
+  if (goal_path && (path_len < 1 || step < 0 || path_stride < 0)) {
+    set_error(h, "gato_mpc_advance: path_len >= 1, step >= 0, path_stride >= 0");
+    return GATO_E_INVALID;
+  }
+  const SolveParams& P = h->P;
+  const size_t bytes = ((size_t)(P.N + 1) * h->ops.nx + (size_t)P.N * h->ops.nu) * sizeof(double);
+  if (bytes > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_mpc_advance, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  }
+  // the caller's buffers are written here: x_start and goal are inputs of the solve, not of this call
+  k_mpc_advance<<<P.M, 128, bytes, static_cast<cudaStream_t>(stream)>>>(
+      P.X, P.U, const_cast<double*>(P.x_start), const_cast<double*>(P.goal), goal_path, path_len, path_stride, step,
+      P.N, h->ops.nx, h->ops.nu);
+  CK(cudaGetLastError());
+  return GATO_OK;
+}
+
 int gato_best_of_batch(gato_handle* h, void* stream, int32_t* best_index, double* best_merit) {
   if (!h || !h->bound) return GATO_E_INVALID;
   k_best_of_batch<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(h->P, best_index, best_merit);

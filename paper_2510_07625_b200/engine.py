@@ -294,6 +294,25 @@ class BatchEngine:
             self.stream.synchronize()
             return int(bi.item()), float(bm.item())
 
+    def mpc_advance(self, goal_path=None, step: int = 0):
+        """One control period on the device, in place (gato_mpc_advance): x_start <- X[:, 1], X and U
+        shifted (mpc.py:85-89) and, with ``goal_path`` (a CUDA float64 tensor [T, n] shared by all solves or
+        [M, T, n]), the goal window advanced to goal_path[step : step + N + 1] (clamped at the end)."""
+        ptr, plen, stride = None, 0, 0
+        if goal_path is not None:
+            if not (goal_path.is_cuda and goal_path.dtype == self.torch.float64 and goal_path.is_contiguous()):
+                raise ValueError("goal_path must be a contiguous CUDA float64 tensor")
+            n = self.shapes["x_start"][1]
+            if goal_path.dim() == 2 and goal_path.shape[1] == n:
+                plen, stride = goal_path.shape[0], 0
+            elif goal_path.dim() == 3 and goal_path.shape[0] == self.M and goal_path.shape[2] == n:
+                plen, stride = goal_path.shape[1], goal_path.shape[1] * n
+            else:
+                raise ValueError(f"goal_path must have shape (T, {n}) or ({self.M}, T, {n})")
+            ptr = C.c_void_p(goal_path.data_ptr())
+        self._check(self.lib.gato_mpc_advance(self.handle, C.c_void_p(self.stream.cuda_stream), ptr, int(plen),
+                                              int(stride), int(step)), "gato_mpc_advance")
+
     def shift_warm_start(self):
         """X, U <- shifted one knot left with the tail duplicated, on the device (mpc.py:85-89)."""
         self._check(self.lib.gato_shift_warm_start(self.handle, C.c_void_p(self.stream.cuda_stream)),

@@ -135,3 +135,36 @@ def test_select_hypothesis_matches_the_plant_rollout(model_name, position_only):
     assert np.max(np.abs(err - want)) <= 1e-11 * max(1.0, want.max())
     with pytest.raises(ValueError):
         gb.select_hypothesis(model, x_prev, u, x_meas, forces, 0.0105, h_plant)
+
+
+def test_mpc_advance_is_the_three_host_steps_in_one_kernel():
+    """gato_mpc_advance: x_start <- X[:, 1], shift (mpc.py:85-89), goal window advanced along a path
+    (shared or per solve, clamped at its end) -- against numpy on the downloaded buffers."""
+    import torch
+    M, N = 5, 9
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, workloads.fixed_budget_settings(1))
+    rng = np.random.default_rng(2)
+    try:
+        first = eng.solve(batch)
+        path = rng.standard_normal((N + 4, 14))
+        eng.mpc_advance(torch.as_tensor(path, device="cuda"), step=2)
+        eng.stream.synchronize()
+        X, U = eng.dev["X"].cpu().numpy(), eng.dev["U"].cpu().numpy()
+        assert np.array_equal(eng.dev["x_start"].cpu().numpy(), first.X[:, 1])
+        assert np.array_equal(X, np.concatenate([first.X[:, 1:], first.X[:, -1:]], axis=1))
+        assert np.array_equal(U, np.concatenate([first.U[:, 1:], first.U[:, -1:]], axis=1))
+        rows = np.minimum(2 + np.arange(N + 1), len(path) - 1)          # clamped at the end of the path
+        assert np.array_equal(eng.dev["goal"].cpu().numpy(), np.broadcast_to(path[rows], (M, N + 1, 14)))
+        per_solve = rng.standard_normal((M, N + 6, 14))
+        eng.mpc_advance(torch.as_tensor(per_solve, device="cuda"), step=0)
+        eng.stream.synchronize()
+        assert np.array_equal(eng.dev["goal"].cpu().numpy(), per_solve[:, :N + 1])
+        goal_before = eng.dev["goal"].clone()
+        eng.mpc_advance()                                                # no path: goals untouched
+        eng.stream.synchronize()
+        assert torch.equal(eng.dev["goal"], goal_before)
+        with pytest.raises(ValueError):
+            eng.mpc_advance(torch.zeros((3, 7), device="cuda", dtype=torch.float64))
+    finally:
+        eng.close()
