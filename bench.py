@@ -362,14 +362,19 @@ def run_gpu_arm(args, w, rank, local_rank, world):
                                                               "rho_init", "X", "U")
     h2d_bytes = sum(getattr(step_inputs, f).nbytes for f in h2d_fields)
 
+    host_in = eng.host_inputs()      # pinned staging buffers of the inputs, written in place
+
     def e2e_step(s):
-        # BatchEngine.step = one gato_solve_host call: pinned H2D of the inputs, (device shift,) solve, D2H
+        # BatchEngine.step = one gato_solve_host call: pinned H2D of the inputs, (device shift,) solve, D2H;
+        # the caller fills the pinned inputs in place and reads the results from the pinned mirror
         if track:
-            step_inputs.goal[...] = ref_path[s:s + N + 1][None]
-            out = eng.step(step_inputs, fields=h2d_fields, shift=True)
-            step_inputs.x_start[...] = out.X[:, 1, :]      # "measured" state for the next control step
+            host_in["goal"][...] = ref_path[s:s + N + 1][None]
+            out = eng.step(None, fields=h2d_fields, shift=True, copy=False)
+            host_in["x_start"][...] = out.X[:, 1, :]       # "measured" state for the next control step
         else:
-            out = eng.step(step_inputs, fields=h2d_fields)
+            for f in h2d_fields:
+                host_in[f][...] = getattr(step_inputs, f)
+            out = eng.step(None, fields=h2d_fields, copy=False)
         return out
 
     for s in range(min(args.warmup, 5)):

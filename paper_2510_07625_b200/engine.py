@@ -251,21 +251,23 @@ class BatchEngine:
 
     STEP_FIELDS = ("x_start", "goal", "force")
 
-    def step(self, batch: PackedBatch, fields=STEP_FIELDS, shift: bool = False, copy: bool = True) -> PackedResult:
+    def step(self, batch: PackedBatch | None, fields=STEP_FIELDS, shift: bool = False,
+             copy: bool = True) -> PackedResult:
         """One control step with host buffers in ONE call across the C ABI (gato_solve_host): the named
         inputs (a contiguous run of the arena; default: the per-step MPC inputs x_start, goal, force) go
         host -> pinned -> device, the warm start is optionally shifted on the device (mpc.py:85-89), the
         solve runs to termination and X, U, trace, info come back.  copy=False returns views of the
         pinned mirror, valid until the next call."""
-        for name in fields:
-            src = getattr(batch, name)
-            if src.shape != self.shapes[name]:
-                raise ValueError(f"{name}: expected shape {self.shapes[name]}, got {src.shape}")
-            self.pin_np[name][...] = src
         order = [n for n in self.layout if n in fields]
         idx = [self.layout.index(n) for n in order]
         if idx != list(range(idx[0], idx[0] + len(idx))):
             raise ValueError("step(): the uploaded fields must be adjacent in the arena; use upload() + launch()")
+        if batch is not None:      # None: the caller has written the inputs into host_inputs() already
+            for name in fields:
+                src = getattr(batch, name)
+                if src.shape != self.shapes[name]:
+                    raise ValueError(f"{name}: expected shape {self.shapes[name]}, got {src.shape}")
+                self.pin_np[name][...] = src
         cin, cout = self._span(order[0], order[-1]), self._span("X", "info")
         base_d, base_h = self.arena.data_ptr(), self.pinned.data_ptr()
         self._check(self.lib.gato_solve_host(
@@ -277,6 +279,11 @@ class BatchEngine:
         get = (lambda a: a.copy()) if copy else (lambda a: a)
         return PackedResult(get(self.pin_np["X"]), get(self.pin_np["U"]), get(self.pin_np["trace"]),
                             get(self.pin_np["info"]), float("nan"))
+
+    def host_inputs(self) -> dict:
+        """Writable numpy views of the pinned staging buffers of the inputs (x_start, goal, force, Q, R, QN,
+        rho_init, X, U): fill them in place and call ``step(None, fields=...)`` to skip one host copy."""
+        return {name: self.pin_np[name] for name in INPUT_FIELDS}
 
     def best_of_batch(self) -> tuple[int, float]:
         """(index, final merit) of the best solve of the last batch, selected on the device
