@@ -147,7 +147,7 @@ def test_loop_modes_agree_bitwise():
 def test_long_horizons_match_the_oracle(model_name, N):
     """BASELINE.json sweep reaches N=128.  The fat-thread PCG kernel has three builds (n=14): O^ blocks
     and packed L resident in shared memory (N=48), O^ resident with L read from L2 for the exact-norm
-    iterations (N=128), and everything in global memory (N=160); the golden cases stop at N=32."""
+    iterations (N=128; up to N=136), and everything in global memory (N=160); the golden cases stop at N=32."""
     from oracle import trajopt_np as orc
     rng = np.random.default_rng(77)
     if model_name == "iiwa14":
