@@ -39,7 +39,7 @@ extern "C" {
 #define GATO_ABI_VERSION 1
 
 /* model ids: the reference's analytic models (dynamics.py:145,190,255,388) + iiwa14 */
-#define GATO_MODEL_DOUBLE_INTEGRATOR 0 /* params: [dims, mass]                                 */
+#define GATO_MODEL_DOUBLE_INTEGRATOR 0 /* params: [dims (1..7), mass]                         */
 #define GATO_MODEL_PENDULUM 1          /* params: [mass, length, gravity, damping]             */
 #define GATO_MODEL_CARTPOLE 2          /* params: [cart_mass, pole_mass, pole_length, gravity] */
 #define GATO_MODEL_TWO_LINK_ARM 3      /* params: [m1, m2, l1, l2, gravity, joint_damping]     */

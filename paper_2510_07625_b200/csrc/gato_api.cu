@@ -27,10 +27,8 @@ bool select_ops(int model_id, const double* params, ModelOps* ops) {
   switch (model_id) {
     case GATO_MODEL_DOUBLE_INTEGRATOR: {
       const int dims = params ? (int)params[0] : 0;
-      if (dims == 1) *ops = gato_ops_double_integrator(1);
-      else if (dims == 2) *ops = gato_ops_double_integrator(2);
-      else if (dims == 7) *ops = gato_ops_double_integrator(7);
-      else return false;
+      if (dims < 1 || dims > 7) return false;
+      *ops = gato_ops_double_integrator(dims);
       return true;
     }
     case GATO_MODEL_PENDULUM: *ops = gato_ops_pendulum(); return true;

@@ -48,7 +48,7 @@ class DynamicsModel:
 
 @dataclass(frozen=True)
 class DoubleIntegrator(DynamicsModel):
-    """dynamics.py:145-163.  Device instantiations exist for dims in {1, 2, 7}."""
+    """dynamics.py:145-163.  Device instantiations exist for dims = 1..7."""
 
     dims: int = 1
     mass: float = 1.0
@@ -128,8 +128,8 @@ def device_model(model) -> tuple[int, np.ndarray]:
     name = getattr(model, "name", None)
     params = np.zeros(8)
     if name == "double_integrator":
-        if model.dims not in (1, 2, 7):
-            raise ValueError("double_integrator is instantiated on the device for dims 1, 2 and 7")
+        if not 1 <= model.dims <= 7:
+            raise ValueError("double_integrator is instantiated on the device for dims 1..7")
         params[:2] = [model.dims, model.mass]
         return MODEL_DOUBLE_INTEGRATOR, params
     if name == "pendulum":

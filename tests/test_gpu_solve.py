@@ -278,3 +278,20 @@ def test_non_finite_initial_guess_behaves_like_the_reference():
         assert got.pcg_iterations == want.pcg_iterations == 10 * 9 * 2
         assert got.rho == want.rho and np.isnan(got.step_inf_norm) and np.isnan(want.step_inf_norm)
     assert np.array_equal(res.X, X, equal_nan=True) and np.array_equal(res.U, U)
+
+
+@pytest.mark.parametrize("dims", [3, 4, 5, 6])
+def test_point_masses_in_every_supported_dimension(dims):
+    """dynamics.py:145-163: DoubleIntegrator(dims) for the dimensions the golden set does not cover,
+    dense random SPD weights, against the numpy oracle."""
+    from oracle import trajopt_np as orc
+    rng = np.random.default_rng(500 + dims)
+    problem, X, U = _random_problem(rng, gb.DoubleIntegrator(dims=dims))
+    st = gb.SolverSettings(max_sqp_iterations=4, step_tolerance=None)
+    res = gb.sqp_solve(problem, X, U, st)
+    ref = orc.solve(orc.Problem.from_spec(problem), X, U, orc.Settings(max_sqp_iterations=4, step_tolerance=None))
+    assert rel_inf(res.X, ref.X) <= 1e-8 and rel_inf(res.U, ref.U) <= 1e-8
+    got, want = trace_rows(res), trace_rows(ref)
+    assert len(got) == len(want) == 4
+    assert np.max(np.abs(got[:, 5] - want[:, 5])) <= 1
+    assert rel_inf(got[:, 1], want[:, 1]) <= 1e-9
