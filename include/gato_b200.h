@@ -8,7 +8,7 @@
  *                                             (M x sqp_solve                sqp.py:204-295)
  *   gato_step_many                            replaces dynamics.step_many           dynamics.py:805-816
  *   gato_step_jacobians_many                  replaces dynamics.step_jacobians_many dynamics.py:774-802
- *   gato_pcg_batched                          replaces blocktri.pcg / btmv          blocktri.py:105-173
+ *   gato_pcg_batched / gato_btmv_batched      replace  blocktri.pcg / btmv          blocktri.py:105-173
  *   gato_shift_warm_start                     replaces mpc.shift_warm_start         mpc.py:85-89
  *   gato_best_of_batch                        replaces the best-of-batch argmin     mpc.py:283-298
  *   gato_select_hypothesis                    replaces mpc.select_hypothesis        mpc.py:130-147
@@ -200,6 +200,10 @@ int gato_select_hypothesis(int32_t model_id, const double* model_params, int32_t
 int gato_step_jacobians_many(int32_t model_id, const double* model_params, int64_t rows,
                              const double* X, const double* U, const double* F, double timestep,
                              double* A, double* B, void* stream);
+/* y = densify(M) v for a batch of symmetric block-tridiagonal matrices stored as diag [nb, bd, bd] +
+ * sub-diagonal [nb-1, bd, bd] blocks (blocktri.py:105-120: diagonal, sub-diagonal, super-diagonal term). */
+int gato_btmv_batched(int32_t systems, int32_t n_blockrows, int32_t block_dim, const double* diag,
+                      const double* off, const double* v, double* y, void* stream);
 /* Batched PCG on explicit block-tridiagonal S and preconditioner Phi^-1 (both stored as
  * diag [nb, bd, bd] + sub-diagonal [nb-1, bd, bd] blocks per system). status: 0 ok,
  * 2 breakdown (iters = breakdown iteration). */

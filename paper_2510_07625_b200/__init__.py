@@ -7,11 +7,13 @@ kernels behind the C ABI in include/gato_b200.h.  There is no CPU execution path
 """
 
 from .batch import BatchSpec, batch_solve, bench_scaling, clear_engine_cache, shard_bounds, sqp_solve
+from .blocktri import BlockTriMatrix, PcgResult, btmv, densify, pcg, step, step_jacobians
 from .engine import (BatchEngine, PackedBatch, PackedResult, pcg_batched, select_hypothesis, step_jacobians_many,
                      step_many)
 from .errors import (BackendUnavailableError, ConfigError, DimensionError, FactorizationError,
                      PcgBreakdownError)
 from .models import Cartpole, DoubleIntegrator, DynamicsModel, Iiwa14, Pendulum, TwoLinkArm
+from .mpc import best_of_batch, rho_grid, sample_hypotheses, shift_warm_start
 from .problem import CostSpec, ExternalForce, ProblemSpec
 from .results import BatchResult, IterationRecord, SqpResult
 from .settings import LineSearchSettings, PcgSettings, SolverSettings
@@ -19,6 +21,8 @@ from .settings import LineSearchSettings, PcgSettings, SolverSettings
 __version__ = "0.1.0"
 
 __all__ = [
+    "BlockTriMatrix", "PcgResult", "btmv", "densify", "pcg", "step", "step_jacobians",
+    "best_of_batch", "rho_grid", "sample_hypotheses", "shift_warm_start",
     "BackendUnavailableError", "BatchEngine", "BatchResult", "BatchSpec", "Cartpole", "ConfigError",
     "CostSpec", "DimensionError", "DoubleIntegrator", "DynamicsModel", "ExternalForce",
     "FactorizationError", "Iiwa14", "IterationRecord", "LineSearchSettings", "PackedBatch",

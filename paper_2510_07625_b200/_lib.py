@@ -69,6 +69,8 @@ EXPORTS = {
     "gato_step_jacobians_many": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int64, C.c_void_p,
                                            C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                            C.c_void_p, C.c_void_p]),
+    "gato_btmv_batched": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p]),
     "gato_pcg_batched": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -163,6 +163,18 @@ __device__ __forceinline__ double bt_row(const double* __restrict__ diag, const 
   return acc;
 }
 
+// k_btmv: y = densify(M) v for a batch of block-tridiagonal matrices (blocktri.py:105-120): one thread per
+// row, terms added in the reference's order (diagonal, sub-diagonal, super-diagonal).
+__global__ void k_btmv(int nb, int bd, const double* __restrict__ diag, const double* __restrict__ off,
+                       const double* __restrict__ v, double* __restrict__ y) {
+  const int sys = blockIdx.y, size = nb * bd;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= size) return;
+  const size_t dstride = (size_t)nb * bd * bd, ostride = (size_t)(nb > 1 ? nb - 1 : 0) * bd * bd;
+  y[(size_t)sys * size + row] =
+      bt_row(diag + sys * dstride, off + sys * ostride, nb, bd, v + (size_t)sys * size, row);
+}
+
 __global__ void __launch_bounds__(256) k_pcg_explicit(int nb, int bd, const double* Sd, const double* So,
                                                       const double* gamma, const double* Pd, const double* Po,
                                                       double tol, int cap, double* lam_out, int32_t* iters,

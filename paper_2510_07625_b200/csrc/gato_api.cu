@@ -633,6 +633,15 @@ int gato_step_jacobians_many(int32_t model_id, const double* model_params, int64
   return err == cudaSuccess ? GATO_OK : GATO_E_CUDA;
 }
 
+int gato_btmv_batched(int32_t systems, int32_t nb, int32_t bd, const double* diag, const double* off, const double* v,
+                      double* y, void* stream) {
+  if (systems < 1 || nb < 1 || bd < 1 || !diag || !v || !y || (nb > 1 && !off)) return GATO_E_INVALID;
+  const int size = nb * bd;
+  dim3 grid((size + 127) / 128, systems);
+  k_btmv<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(nb, bd, diag, off, v, y);
+  return cudaGetLastError() == cudaSuccess ? GATO_OK : GATO_E_CUDA;
+}
+
 int gato_pcg_batched(int32_t systems, int32_t nb, int32_t bd, const double* S_diag, const double* S_off,
                      const double* gamma, const double* P_diag, const double* P_off, double tolerance,
                      int32_t max_iterations, double* lam, int32_t* iterations, int32_t* converged, int32_t* status,

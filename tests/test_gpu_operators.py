@@ -134,3 +134,55 @@ def test_shift_warm_start_on_device():
         eng.close()
     assert np.array_equal(X, np.concatenate([batch.X[:, 1:], batch.X[:, -1:]], axis=1))
     assert np.array_equal(U, np.concatenate([batch.U[:, 1:], batch.U[:, -1:]], axis=1))
+
+
+def test_reference_named_blocktri_operators(rng):
+    """BlockTriMatrix / btmv / pcg / PcgResult / densify with the reference's signatures and checks
+    (blocktri.py:19-173; test_blocktri.py patterns: dense cross-check, identity -> 1 iteration, zero rhs -> 0,
+    dimension errors, breakdown on a non-SPD system)."""
+    nb, bd = 6, 4
+    W = rng.standard_normal((nb, bd, bd))
+    diag = W @ W.transpose(0, 2, 1) + 6.0 * np.eye(bd)
+    off = 0.3 * rng.standard_normal((nb - 1, bd, bd))
+    S = gb.BlockTriMatrix(diag, off)
+    v = rng.standard_normal(nb * bd)
+    assert rel_inf(gb.btmv(S, v), gb.densify(S) @ v) <= 1e-13
+    P = gb.BlockTriMatrix(np.linalg.inv(diag), np.zeros_like(off))          # block-Jacobi preconditioner
+    gamma = rng.standard_normal(nb * bd)
+    out = gb.pcg(S, gamma, P, gb.PcgSettings(tolerance=1e-10))
+    assert isinstance(out, gb.PcgResult) and out.converged and out.final_residual_norm <= 1e-10
+    assert rel_inf(out.solution, np.linalg.solve(gb.densify(S), gamma)) <= 1e-9
+    eye = gb.BlockTriMatrix.identity(3, 2)
+    one = gb.pcg(eye, np.arange(6.0) + 1.0, eye, gb.PcgSettings())
+    assert one.iterations == 1 and one.converged
+    assert gb.pcg(eye, np.zeros(6), eye, gb.PcgSettings()).iterations == 0
+    with pytest.raises(gb.DimensionError):
+        gb.btmv(S, np.zeros(3))
+    with pytest.raises(gb.DimensionError):
+        gb.BlockTriMatrix(diag, off[:-1])
+    neg = gb.BlockTriMatrix(-np.tile(np.eye(2), (3, 1, 1)), np.zeros((2, 2, 2)))
+    with pytest.raises(gb.PcgBreakdownError) as info:
+        gb.pcg(neg, np.ones(6), eye, gb.PcgSettings())
+    assert info.value.iteration == 1
+
+
+def test_scalar_step_and_jacobians_follow_the_reference_contract():
+    """dynamics.py:716-772: shape and finiteness checks, force vectors or ExternalForce objects."""
+    model = gb.Pendulum()
+    x, u = np.array([0.3, -0.2]), np.array([0.5])
+    out = gb.step(model, x, u, 0.05)
+    A, B = gb.step_jacobians(model, x, u, 0.05, gb.ExternalForce.constant([0.1]))
+    assert out.shape == (2,) and A.shape == (2, 2) and B.shape == (2, 1)
+    eps = 1e-6
+    fd = (gb.step(model, x + [eps, 0], u, 0.05, [0.1]) - gb.step(model, x - [eps, 0], u, 0.05, [0.1])) / (2 * eps)
+    assert np.max(np.abs(A[:, 0] - fd)) <= 1e-8
+    with pytest.raises(ValueError):
+        gb.step(model, np.array([np.nan, 0.0]), np.zeros(1), 0.05)
+    with pytest.raises(ValueError):
+        gb.step(model, np.zeros(2), np.array([np.inf]), 0.05)
+    with pytest.raises(gb.DimensionError):
+        gb.step(model, np.zeros(3), np.zeros(1), 0.05)
+    with pytest.raises(gb.DimensionError):
+        gb.step(model, np.zeros(2), np.zeros(1), 0.05, [0.0, 0.0])
+    with pytest.raises(ValueError):
+        gb.step(model, np.zeros(2), np.zeros(1), 0.0)
