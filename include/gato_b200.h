@@ -10,6 +10,7 @@
  *   gato_step_jacobians_many                  replaces dynamics.step_jacobians_many dynamics.py:774-802
  *   gato_pcg_batched / gato_btmv_batched      replace  blocktri.pcg / btmv          blocktri.py:105-173
  *   gato_shift_warm_start                     replaces mpc.shift_warm_start         mpc.py:85-89
+ *   gato_merit_candidates                     replaces sqp.merit / merit_many       sqp.py:111-166
  *   gato_best_of_batch                        replaces the best-of-batch argmin     mpc.py:283-298
  *   gato_select_hypothesis                    replaces mpc.select_hypothesis        mpc.py:130-147
  *   gato_solve_host / gato_mpc_advance        one control step of _MpcEngine.advance mpc.py:240-274
@@ -152,6 +153,11 @@ int gato_mpc_advance(gato_handle* h, void* stream, const double* goal_path, int6
  * with gato_bind); either copy may be skipped with 0 bytes. */
 int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host_in, int64_t in_bytes,
                     int32_t shift_first, const void* dev_out, void* host_out, int64_t out_bytes);
+/* Merit evaluation alone (sqp.py:111-166): for every solve of the bound batch, the L1 merit of the
+ * candidates (X + alpha_c dX, U + alpha_c dU), alpha_c = beta^-c, c = 0..num_shrinks, and of the current
+ * iterate itself. dX [M, N+1, n], dU [M, N, m]: device arrays (null = zero step). Results in the scratch
+ * arrays "merits" / "viols" ([M, num_shrinks + 2]: the candidates, then alpha = 0). Asynchronous. */
+int gato_merit_candidates(gato_handle* h, void* stream, const double* dX, const double* dU);
 /* Best-of-batch selection on the device (mpc.py:283-298): index of the solve with the lowest final
  * merit among the solves without a failure status, first minimum on ties, -1 if every solve failed;
  * written to the device words *best_index / *best_merit (either may be null). Asynchronous. */

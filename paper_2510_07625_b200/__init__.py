@@ -12,6 +12,7 @@ from .engine import (BatchEngine, PackedBatch, PackedResult, pcg_batched, select
                      step_many)
 from .errors import (BackendUnavailableError, ConfigError, DimensionError, FactorizationError,
                      PcgBreakdownError)
+from .merit import adapt_rho, constraint_l1, line_search, merit, merit_many
 from .models import Cartpole, DoubleIntegrator, DynamicsModel, Iiwa14, Pendulum, TwoLinkArm
 from .mpc import best_of_batch, rho_grid, sample_hypotheses, shift_warm_start
 from .problem import CostSpec, ExternalForce, ProblemSpec
@@ -23,6 +24,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BlockTriMatrix", "PcgResult", "btmv", "densify", "pcg", "step", "step_jacobians",
     "best_of_batch", "rho_grid", "sample_hypotheses", "shift_warm_start",
+    "adapt_rho", "constraint_l1", "line_search", "merit", "merit_many",
     "BackendUnavailableError", "BatchEngine", "BatchResult", "BatchSpec", "Cartpole", "ConfigError",
     "CostSpec", "DimensionError", "DoubleIntegrator", "DynamicsModel", "ExternalForce",
     "FactorizationError", "Iiwa14", "IterationRecord", "LineSearchSettings", "PackedBatch",

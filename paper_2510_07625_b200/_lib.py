@@ -48,6 +48,7 @@ EXPORTS = {
     "gato_shift_warm_start": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gato_solve_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_int64]),
+    "gato_merit_candidates": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gato_best_of_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gato_mpc_advance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64]),
     "gato_pending": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),

@@ -415,6 +415,21 @@ int gato_mpc_advance(gato_handle* h, void* stream, const double* goal_path, int6
   return GATO_OK;
 }
 
+int gato_merit_candidates(gato_handle* h, void* stream, const double* dX, const double* dU) {
+  if (!h || !h->bound) return GATO_E_INVALID;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const SolveParams& P = h->P;
+  const size_t nX = (size_t)P.M * (P.N + 1) * h->ops.nx * sizeof(double), nU = (size_t)P.M * P.N * h->ops.nu * sizeof(double);
+  if (dX) CK(cudaMemcpyAsync(P.dX, dX, nX, cudaMemcpyDeviceToDevice, s));
+  else CK(cudaMemsetAsync(P.dX, 0, nX, s));
+  if (dU) CK(cudaMemcpyAsync(P.dU, dU, nU, cudaMemcpyDeviceToDevice, s));
+  else CK(cudaMemsetAsync(P.dU, 0, nU, s));
+  int rc = enqueue_prologue(h, s);   // every solve active, merit of the current iterate not yet known
+  if (rc != GATO_OK) return rc;
+  CK(h->ops.linesearch(P, s));
+  return GATO_OK;
+}
+
 int gato_best_of_batch(gato_handle* h, void* stream, int32_t* best_index, double* best_merit) {
   if (!h || !h->bound) return GATO_E_INVALID;
   k_best_of_batch<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(h->P, best_index, best_merit);

@@ -285,6 +285,26 @@ class BatchEngine:
         rho_init, X, U): fill them in place and call ``step(None, fields=...)`` to skip one host copy."""
         return {name: self.pin_np[name] for name in INPUT_FIELDS}
 
+    def merit_candidates(self, dX=None, dU=None):
+        """(merits, violations), each (M, num_shrinks + 2): the L1 merit (sqp.py:118-166) of the candidates
+        X + beta^-c dX, c = 0..num_shrinks, followed by the merit of the uploaded iterate itself, evaluated
+        by the line-search kernel alone (gato_merit_candidates).  dX, dU: host arrays or None (zero step)."""
+        torch = self.torch
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            ddx = None if dX is None else torch.as_tensor(np.ascontiguousarray(dX, dtype=float)).to(self.device)
+            ddu = None if dU is None else torch.as_tensor(np.ascontiguousarray(dU, dtype=float)).to(self.device)
+            if ddx is not None and tuple(ddx.shape) != self.shapes["X"]:
+                raise ValueError(f"dX: expected shape {self.shapes['X']}")
+            if ddu is not None and tuple(ddu.shape) != self.shapes["U"]:
+                raise ValueError(f"dU: expected shape {self.shapes['U']}")
+            self._check(self.lib.gato_merit_candidates(
+                self.handle, C.c_void_p(self.stream.cuda_stream),
+                C.c_void_p(ddx.data_ptr()) if ddx is not None else None,
+                C.c_void_p(ddu.data_ptr()) if ddu is not None else None), "gato_merit_candidates")
+        self.stream.synchronize()
+        width = self.settings.line_search.num_shrinks + 2
+        return self.scratch("merits").reshape(self.M, width), self.scratch("viols").reshape(self.M, width)
+
     def best_of_batch(self) -> tuple[int, float]:
         """(index, final merit) of the best solve of the last batch, selected on the device
         (gato_best_of_batch; mpc.py:283-298): lowest final merit among the solves that did not fail,

@@ -186,3 +186,49 @@ def test_scalar_step_and_jacobians_follow_the_reference_contract():
         gb.step(model, np.zeros(2), np.zeros(1), 0.05, [0.0, 0.0])
     with pytest.raises(ValueError):
         gb.step(model, np.zeros(2), np.zeros(1), 0.0)
+
+
+def test_reference_named_merit_and_line_search_operators(rng):
+    """sqp.merit / merit_many / constraint_l1 / line_search / adapt_rho with the reference's signatures
+    (sqp.py:111-201) and its test patterns: the merit = 7.5 known answer (test_sqp.py:44-53), the L1 term
+    includes the initial-state row (test_sqp.py:289-296), non-finite candidates score +inf, batched equals
+    single, the candidate set and the strict-decrease rule, the rho clamps (test_sqp.py:165-179)."""
+    from oracle import trajopt_np as orc
+    # double integrator, N = 2: a trajectory that is feasible except for the start state
+    model = gb.DoubleIntegrator(dims=1)
+    cost = gb.CostSpec(Q=np.eye(2), R=np.eye(1), QN=np.eye(2), goal=np.zeros(2))
+    problem = gb.ProblemSpec(model=model, cost=cost, horizon=2, timestep=0.1, x_start=np.array([1.0, 0.0]))
+    X = np.zeros((3, 2))
+    U = np.zeros((2, 1))
+    assert gb.constraint_l1(problem, X, U) == 1.0                  # only |x_start - x_0|
+    assert gb.merit(problem, X, U, 7.5) == 7.5                     # zero cost + mu * 1
+    # random cartpole trajectories against the oracle
+    cart = gb.ProblemSpec(model=gb.Cartpole(), cost=gb.CostSpec(Q=np.diag([1.0, 2.0, 0.1, 0.1]), R=np.eye(1) * 0.1,
+                                                               QN=5.0 * np.eye(4), goal=np.array([0.0, np.pi, 0, 0])),
+                          horizon=6, timestep=0.05, x_start=0.1 * rng.standard_normal(4),
+                          force=gb.ExternalForce.constant(0.3 * np.ones(gb.Cartpole().force_dim)))
+    Xs, Us = 0.3 * rng.standard_normal((5, 7, 4)), 0.3 * rng.standard_normal((5, 6, 1))
+    op = orc.Problem.from_spec(cart)
+    want = np.array([orc.merit_value(op, Xs[c], Us[c], 10.0) for c in range(5)])
+    got = gb.merit_many(cart, Xs, Us, 10.0)
+    assert rel_inf(got, want) <= 1e-12
+    assert abs(gb.merit(cart, Xs[2], Us[2], 10.0) - got[2]) <= 1e-12 * abs(got[2])
+    assert abs(gb.constraint_l1(cart, Xs[1], Us[1]) - orc.violation_l1(op, Xs[1], Us[1])) <= 1e-12
+    bad = Xs.copy()
+    bad[1, 0, 0] = np.nan
+    bad[3, 2, 1] = np.inf
+    vals = gb.merit_many(cart, bad, Us, 10.0)
+    assert np.isinf(vals[1]) and np.isinf(vals[3]) and rel_inf(vals[[0, 2, 4]], want[[0, 2, 4]]) <= 1e-12
+    # line search: candidate set, first minimum, strict decrease
+    ls = gb.LineSearchSettings(mu=10.0, beta=2.0, num_shrinks=3)
+    assert np.array_equal(ls.candidates(), [1.0, 0.5, 0.25, 0.125])
+    dX, dU = 0.2 * rng.standard_normal((7, 4)), 0.2 * rng.standard_normal((6, 1))
+    ost = orc.Settings(mu=10.0, beta=2.0, num_shrinks=3)
+    a_ref, m_ref, acc_ref, _ = orc.line_search(op, Xs[0], Us[0], dX, dU, ost, orc.merit_value(op, Xs[0], Us[0], 10.0))
+    a, m, acc = gb.line_search(cart, Xs[0], Us[0], dX, dU, ls)
+    assert a == a_ref and acc == acc_ref and abs(m - m_ref) <= 1e-12 * abs(m_ref)
+    a0, m0, acc0 = gb.line_search(cart, Xs[0], Us[0], np.zeros_like(dX), np.zeros_like(dU), ls)
+    assert a0 == 1.0 and acc0 is False                            # a zero step never strictly decreases
+    st = gb.SolverSettings()
+    assert gb.adapt_rho(1e-3, True, st) == 2e-4 and gb.adapt_rho(1e-3, False, st) == 5e-3
+    assert gb.adapt_rho(st.rho_min, True, st) == st.rho_min and gb.adapt_rho(st.rho_max, False, st) == st.rho_max
