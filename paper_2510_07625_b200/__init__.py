@@ -18,6 +18,7 @@ from .mpc import best_of_batch, rho_grid, sample_hypotheses, shift_warm_start
 from .problem import CostSpec, ExternalForce, ProblemSpec
 from .results import BatchResult, IterationRecord, SqpResult
 from .settings import LineSearchSettings, PcgSettings, SolverSettings
+from .stages import KnotLinearization, SchurSystem, StageDump, StepDirection, first_iteration_stages
 
 __version__ = "0.1.0"
 
@@ -25,6 +26,7 @@ __all__ = [
     "BlockTriMatrix", "PcgResult", "btmv", "densify", "pcg", "step", "step_jacobians",
     "best_of_batch", "rho_grid", "sample_hypotheses", "shift_warm_start",
     "adapt_rho", "constraint_l1", "line_search", "merit", "merit_many",
+    "KnotLinearization", "SchurSystem", "StageDump", "StepDirection", "first_iteration_stages",
     "BackendUnavailableError", "BatchEngine", "BatchResult", "BatchSpec", "Cartpole", "ConfigError",
     "CostSpec", "DimensionError", "DoubleIntegrator", "DynamicsModel", "ExternalForce",
     "FactorizationError", "Iiwa14", "IterationRecord", "LineSearchSettings", "PackedBatch",

@@ -97,3 +97,25 @@ def test_whitened_preconditioner_equals_explicit_stair_blocks(name):
         eng.close()
     explicit = np.stack([-D[k + 1] @ off[k] @ D[k] for k in range(N)])
     assert rel_inf(explicit, g["Poff"]) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["cartpole_n8", "iiwa14_reach_n8_b0", "twolink_profile_n8"])
+def test_first_iteration_stages_in_the_reference_types(name):
+    """first_iteration_stages: the reference's linearize -> form_schur -> form_preconditioner -> pcg ->
+    recover_step -> merit_many chain as reference-typed objects, against the golden stages."""
+    g = load_golden(name)
+    problem, st = product_problem(g), product_settings(g)
+    N, n, m = problem.horizon, problem.model.state_dim, problem.model.control_dim
+    d = gb.first_iteration_stages(problem, g["X0"], g["U0"], st)
+    assert len(d.blocks) == N + 1 and d.blocks[-1].A is None and d.blocks[-1].R is None
+    assert rel_inf(np.stack([b.A for b in d.blocks[:-1]]), g["A"]) <= 1e-11
+    assert rel_inf(np.stack([b.q for b in d.blocks]), g["q"]) <= 1e-12
+    assert np.array_equal(d.blocks[0].Q, g["Q"] + st.rho_init * np.eye(n))     # damped Hessian, undamped gradient
+    assert rel_inf(d.system.S.diag_blocks, g["Sdiag"]) <= 1e-11 and rel_inf(d.system.phi, g["Soff"]) <= 1e-11
+    assert rel_inf(d.system.gamma, g["gamma"]) <= 1e-11 and rel_inf(d.system.q_inv, g["q_inv"]) <= 1e-11
+    assert rel_inf(d.system.phi_inv.diag_blocks, g["Pdiag"]) <= 1e-9
+    assert rel_inf(d.system.phi_inv.offdiag_blocks, g["Poff"]) <= 1e-9
+    assert abs(d.pcg.iterations - int(g["pcg_iterations"])) <= 1 and d.pcg.converged == bool(g["pcg_converged"])
+    assert rel_inf(d.pcg.solution, g["lam"]) <= 1e-8
+    assert rel_inf(d.direction.dX, g["dX"]) <= 1e-7 and abs(d.direction.inf_norm - float(g["step_inf"])) <= 1e-7
+    assert rel_inf(d.merits, g["merits"]) <= 1e-8 and abs(d.merit0 - float(g["merit0"])) <= 1e-9 * abs(float(g["merit0"]))
