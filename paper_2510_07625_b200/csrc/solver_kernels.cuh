@@ -63,6 +63,15 @@ struct SpdScratch {
   double col[2][D + (D & 1)];    // the pivot column being eliminated, double buffered
 };
 
+// (row, column) of entry p of a packed lower triangle: p = row (row + 1) / 2 + column, column <= row
+__device__ __forceinline__ void tri_coords(int p, int& row, int& col) {
+  int i = (int)((sqrtf(8.0f * (float)p + 1.0f) - 1.0f) * 0.5f);
+  if ((i + 1) * (i + 2) / 2 <= p) ++i;
+  if (i * (i + 1) / 2 > p) --i;
+  row = i;
+  col = p - i * (i + 1) / 2;
+}
+
 // lower Cholesky factor of the D*D matrix in W -> S.L (row stride D + 1, lower triangle), S.invd;
 // returns 0 or the 1-based index of the failing pivot (pivot <= 0).  A NaN pivot passes, as it does in
 // the reference's scipy.linalg.cho_factor over OpenBLAS (whose potrf, unlike netlib's, has no DISNAN
@@ -80,9 +89,8 @@ __device__ __forceinline__ int warp_cholesky(const double* W, SpdScratch<D>& S, 
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int p = lane + 32 * e;
-    int i = 0;
-    while ((i + 1) * (i + 2) / 2 <= p) ++i;
-    const int k = p - i * (i + 1) / 2;
+    int i, k;
+    tri_coords(p, i, k);
     const bool ok = p < TRI;
     ei[e] = ok ? i : -1;
     ek[e] = ok ? k : -1;
@@ -751,6 +759,31 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_schur(SolveParams P) {
   double* grad = P.grad + ((size_t)b * nb + k) * (NX + NU);
   double* pm = P.pmats + (size_t)b * L::mat_doubles(P.N);
 
+  // the big inputs of this block row (A_{k-1}, B_{k-1}, Q^-1, R^-1) are requested first, so that their
+  // L2 / HBM latency overlaps the gradient section below
+  constexpr int RA = (NX * NX + 31) / 32, RB = (NX * NU + 31) / 32, RR = (NU * NU + 31) / 32;
+  double va[RA], vq[RA], vb[RB], vr[RR];
+  if (k > 0) {
+    const double* Ag = P.A + ((size_t)b * P.N + k - 1) * NX * NX;
+    const double* Bg = P.B + ((size_t)b * P.N + k - 1) * NX * NU;
+#pragma unroll
+    for (int i = 0; i < RA; ++i) {
+      const int idx = lane + 32 * i;
+      va[i] = (idx < NX * NX) ? Ag[idx] : 0.0;
+      vq[i] = (idx < NX * NX) ? Qi[idx] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int idx = lane + 32 * i;
+      vb[i] = (idx < NX * NU) ? Bg[idx] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+      const int idx = lane + 32 * i;
+      vr[i] = (idx < NU * NU) ? Ri[idx] : 0.0;
+    }
+  }
+
   // gradients with the undamped weights (qpform.py:185-186,195)
   if (lane < NX) {
     S.dxk[lane] = Xb[k * NX + lane] - Gb[k * NX + lane];
@@ -807,27 +840,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_schur(SolveParams P) {
     }
   } else {
     const int j = k - 1;
-    const double* Ag = P.A + ((size_t)b * P.N + j) * NX * NX;
-    const double* Bg = P.B + ((size_t)b * P.N + j) * NX * NU;
-    {   // stage A, A^T, Q^-1, B, B^T, R^-1: all global loads issued before the first use
-      constexpr int RA = (NX * NX + 31) / 32, RB = (NX * NU + 31) / 32, RR = (NU * NU + 31) / 32;
-      double va[RA], vq[RA], vb[RB], vr[RR];
-#pragma unroll
-      for (int i = 0; i < RA; ++i) {
-        const int idx = lane + 32 * i;
-        va[i] = (idx < NX * NX) ? Ag[idx] : 0.0;
-        vq[i] = (idx < NX * NX) ? Qi[idx] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < RB; ++i) {
-        const int idx = lane + 32 * i;
-        vb[i] = (idx < NX * NU) ? Bg[idx] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < RR; ++i) {
-        const int idx = lane + 32 * i;
-        vr[i] = (idx < NU * NU) ? Ri[idx] : 0.0;
-      }
+    {   // stage A, A^T, Q^-1, B, B^T, R^-1 (loaded into registers at the top of the kernel)
 #pragma unroll
       for (int i = 0; i < RA; ++i) {
         const int idx = lane + 32 * i;
@@ -945,16 +958,14 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_schur(SolveParams P) {
   double* LfP = LiP + (size_t)nb * L::TRP;
   double* Li = P.Linv + ((size_t)b * nb + k) * TRI;
   double* Lf = P.Lfac + ((size_t)b * nb + k) * TRI;
-  for (int idx = lane; idx < NX * NX; idx += 32) {
-    const int rr = idx / NX, cc = idx % NX;
-    if (cc <= rr) {
-      const int pk = rr * (rr + 1) / 2 + cc;
-      const double vi = S.W[idx], vf = S.spd.L[rr * (NX + 1) + cc];
-      Li[pk] = vi;
-      LiP[pk] = vi;
-      Lf[pk] = vf;
-      LfP[pk] = vf;
-    }
+  for (int pk = lane; pk < TRI; pk += 32) {   // packed index = entry number: coalesced, no div / mod
+    int rr, cc;
+    tri_coords(pk, rr, cc);
+    const double vi = S.W[rr * NX + cc], vf = S.spd.L[rr * (NX + 1) + cc];
+    Li[pk] = vi;
+    LiP[pk] = vi;
+    Lf[pk] = vf;
+    LfP[pk] = vf;
   }
   if (lane < NX) {   // gamma^_k
     double acc = 0.0;
