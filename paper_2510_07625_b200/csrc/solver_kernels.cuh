@@ -105,7 +105,11 @@ __device__ __forceinline__ int warp_cholesky(const double* W, SpdScratch<D>& S, 
       fail = j + 1;
       break;
     }
-    const double r = sqrt(d), ir = rsqrt(d);
+    // r = sqrt(d) from the reciprocal root: d * rsqrt(d) refined by one Newton step (the software sqrt
+    // would cost as much again as the rsqrt on the serial path of every pivot)
+    const double ir = rsqrt(d);
+    double r = d * ir;
+    r = fma(0.5 * ir, fma(-r, r, d), r);
     double* col = S.col[j & 1];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
