@@ -435,9 +435,11 @@ def run_gpu_arm(args, w, rank, local_rank, world):
         fam_ms = {"linearize": kern_ms["linearize"], "schur": kern_ms["schur"] + kern_ms["hessinv"],
                   "pcg": kern_ms["pcg"], "linesearch": kern_ms["linesearch"]}
         dominant = max(fam_ms, key=fam_ms.get)
-        # the PCG family runs the register-resident kernel at short horizons (model_ops.cuh: pcg_use_rt)
-        kernel_names = {"linearize": "k_lin_tangent_iiwa", "schur": "k_schur",
-                        "pcg": "k_pcg_rt" if (N + 1) * 7 <= 256 else "k_pcg", "linesearch": "k_linesearch"}
+        # the PCG family (model_ops.cuh: launch_pcg): rows of O^ in registers at short horizons, quadrants of
+        # O^ in registers up to N = 64, one thread per block row above
+        pcg_kernel = "k_pcg_rt" if (N + 1) * 7 <= 256 else "k_pcg_q" if N <= 64 else "k_pcg"
+        kernel_names = {"linearize": "k_lin_tangent_iiwa", "schur": "k_schur", "pcg": pcg_kernel,
+                        "linesearch": "k_linesearch"}
         launches_dom = K_sqp
         achieved = fam_flops[dominant] / (fam_ms[dominant] * 1e-3) / 1e12
         total_flops = float(np.sum([flops_solve_iteration(N, p) for p in P_prof.reshape(-1)]))

@@ -86,6 +86,16 @@ bool pcg_use_rt(int N) {
          pcg_rt_smem_bytes<Mdl::NX>(N) <= kMaxSmem;
 }
 
+// quad variant (one quadrant of O^_k per thread, in registers) for horizons up to 64; GATO_PCG_Q=0 disables,
+// GATO_PCG_Q=2 prefers it over the real-time variant as well
+template <class Mdl>
+int pcg_use_q(int N) {
+  static int mode = -1;
+  if (mode < 0) mode = env_int("GATO_PCG_Q", 1);
+  if (Mdl::NX < 14 || N < 1 || pcg_q_threads(N) > kPcgQMaxThreads || pcg_q_smem_bytes<Mdl::NX>(N) > kMaxSmem) return 0;
+  return mode;
+}
+
 // Shapes of the fat-thread PCG kernel: O^ blocks in shared memory when they fit, with the packed L_k
 // resident beside them (one CTA per SM); GATO_PCG_MINB=2 selects the two-CTAs-per-SM build instead
 // (shared memory <= 113 KB, <= 128 threads, L_k read from L2 in the few exact-norm iterations).
@@ -137,7 +147,13 @@ template <class Mdl>
 cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU;
   if constexpr (NX >= 14) {
-    if (pcg_use_rt<Mdl>(P.N)) {
+    const int qmode = pcg_use_q<Mdl>(P.N);
+    const bool rt = pcg_use_rt<Mdl>(P.N);
+    if (qmode == 2 || (qmode == 1 && !rt)) {
+      k_pcg_q<NX, NU><<<P.M, pcg_q_threads(P.N), pcg_q_smem_bytes<NX>(P.N), s>>>(P);
+      return cudaGetLastError();
+    }
+    if (rt) {
       k_pcg_rt<NX, NU><<<P.M, pcg_rt_threads(P.N, NX), pcg_rt_smem_bytes<NX>(P.N), s>>>(P);
       return cudaGetLastError();
     }
@@ -207,6 +223,11 @@ cudaError_t prepare_attrs(const SolveParams& P) {
     if (err != cudaSuccess) return err;
   }
   if constexpr (NX >= 14) {
+    if (pcg_use_q<Mdl>(P.N)) {
+      err = cudaFuncSetAttribute(k_pcg_q<NX, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pcg_q_smem_bytes<NX>(P.N));
+      if (err != cudaSuccess) return err;
+    }
     if (pcg_rt_smem_bytes<NX>(P.N) <= kMaxSmem) {
       err = cudaFuncSetAttribute(k_pcg_rt<NX, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pcg_rt_smem_bytes<NX>(P.N));

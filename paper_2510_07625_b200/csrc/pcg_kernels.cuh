@@ -21,6 +21,8 @@
 //   k_pcg_rt  (n = 14, N <= 35: the real-time regime)  thread (k, i) owns rows i and i + n/2 of block
 //             row k; its rows of O^_{k-1}, of O^_k^T and of L_k live in REGISTERS for the whole solve;
 //             shared memory carries only the two exchange vectors.
+//   k_pcg_q   (n = 14, N <= 64)  four threads per block O^_k, one quadrant each in REGISTERS, one pass
+//             over it serving both products; one 7-shuffle round inside the quad completes the sums.
 //   k_pcg     (any n, N + 1 <= 256)  one thread per block row, O^ and L in shared memory (or global
 //             memory when the horizon does not fit), 16-byte row loads, O^_k^T applied by rows.
 #pragma once
@@ -829,6 +831,371 @@ __global__ void __launch_bounds__(MAXT, MINB) k_pcg(SolveParams P) {
     for (int il = 0; il < RP; ++il) {
       dX[il] = dx[il];
       step_part = nanmax(step_part, fabs(dx[il]));
+    }
+  }
+  const double step_inf = R.max1(step_part);
+  if (t == 0) pcg_finish(P, b, si, its, step_inf, viol);
+}
+
+// -----------------------------------------------------------------------------------------
+// k_pcg_q: FOUR threads per block O^_k, each with one (n/2 x n/2) quadrant of it in REGISTERS for the
+// whole solve (n = 14: 49 doubles).  Thread (a, c) of quad k holds Q = O^_k[rows a-half, cols c-half]
+// and one pass over Q serves both products, every element used twice from registers:
+//     up[i] = sum_j Q[i][j] v_k[c-half][j]        partial of u_k = O^_k v_k        (rows a-half)
+//     wp[j] = sum_i Q[i][j] v_{k+1}[a-half][i]    partial of w_k = O^_k^T v_{k+1}  (cols c-half)
+// so a thread loads n shared-memory doubles for n^2/2 FMAs (the fat-thread kernel: one 16-byte load per
+// two FMAs, which bound it by the shared-memory pipe with one warp per scheduler).  ONE round of
+// n/2 64-bit shuffles inside the quad completes both sums: lanes 0 and 3 of the quad end up with the
+// halves of u_k, lanes 2 and 1 with the halves of w_k -- and these two lanes are the owners of the
+// two halves of block row k (lam^, r^, p^ in registers).  u_k travels to the owners of row k+1 through
+// shared memory under the barrier of the reduction; the last block row N (no block of its own) is
+// owned by lanes 0 and 3 of quad N-1, which already hold u_{N-1} in registers.  4 N threads: N = 64
+// fills exactly eight warps, two per scheduler.  Shared memory keeps only the two exchange vectors,
+// the packed L_k for the few exact-norm iterations (see k_pcg) and, before the loop, the record.
+// Half-vectors sit in slots of HP = 10 doubles so the 16-byte loads of a quarter-warp hit distinct banks.
+// -----------------------------------------------------------------------------------------
+constexpr int kPcgQMaxThreads = 256;
+__host__ __device__ constexpr int pcg_q_hp(int NX) { return ((NX / 2 + 1) & ~1) + 2; }
+// (a full CTA for short horizons, its spare warps sharing the one-time row loops, was measured: slower --
+// the idle warps cost more at the barriers than they save before and after the loop)
+__host__ __device__ constexpr int pcg_q_threads(int N) { return (4 * N + 31) / 32 * 32; }
+template <int NX>
+__host__ __device__ constexpr size_t pcg_q_smem_bytes(int N) {
+  const size_t xch = 2 * (size_t)(N + 1) * 2 * pcg_q_hp(NX) * 8;
+  const size_t mats = ((size_t)N * PcgLayout<NX>::BSP + (size_t)(N + 1) * PcgLayout<NX>::TRP) * 8;
+  const size_t vecs = 3 * (size_t)((N + 1) * NX + 2) * 8;
+  return 16 * 16 + xch + (mats > vecs ? mats : vecs);
+}
+
+template <int NX, int NU>
+__global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
+  static_assert(NX % 2 == 0, "state = [positions, velocities]");
+  using L = PcgLayout<NX>;
+  constexpr int HN = NX / 2, BS = NX * NX, HP = pcg_q_hp(NX);
+  constexpr int HS = hinv_stride(NX, NU);
+  const int b = blockIdx.x;
+  int32_t* si = P.si + b * SI_WORDS;
+  if (!si[SI_ACTIVE]) return;
+  if (pcg_schur_failed(P, b, si)) return;
+  const int N = P.N, nb = N + 1;
+  const int t = threadIdx.x;
+  extern __shared__ __align__(16) double pcg_smem[];
+  const int vlen = nb * NX;
+  double2* red = reinterpret_cast<double2*>(pcg_smem);
+  double* xv = reinterpret_cast<double*>(red + 16);   // published vector, slot (row, half) of HP doubles
+  double* xu = xv + (size_t)nb * 2 * HP;              // u_k for the owners of row k+1, same slots
+  double* mats = xu + (size_t)nb * 2 * HP;
+  double* pm = P.pmats + (size_t)b * L::mat_doubles(N);
+  const double* LiG = pm + (size_t)N * L::BSP;          // packed L_k^-1 (global)
+  const double* LfG = LiG + (size_t)nb * L::TRP;        // packed L_k (global)
+  double* Wm = mats;                                    // W_k -> O^_k
+  const double* LfS = mats + (size_t)N * L::BSP;        // packed L_k (shared)
+  __shared__ __align__(8) unsigned long long fill_bar;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&fill_bar);
+  if (t == 0) mbar_init(bar);
+  if (t < 16) red[t] = make_double2(0.0, 0.0);
+  __syncthreads();
+  if (t == 0) {
+    const unsigned bytes_off = (unsigned)((size_t)N * L::BSP * 8), bytes_tri = (unsigned)((size_t)nb * L::TRP * 8);
+    mbar_expect(bar, bytes_off + bytes_tri);
+    bulk_fill_issue(bar, mats, pm, bytes_off);
+    bulk_fill_issue(bar, mats + (size_t)N * L::BSP, LfG, bytes_tri);
+  }
+  const int quad = t >> 2, q = t & 3, qa = q >> 1, qc = q & 1;
+  const bool has_blk = quad < N;
+  const int k = has_blk ? quad : 0;
+  const bool isw = (q == 1) || (q == 2);                 // ends up with a half of w_k (else: of u_k)
+  const bool hold = has_blk && (isw || quad == N - 1);   // owns a half block row
+  const int hk = isw ? k : N, hh = isw ? qc : qa;        // ... this one
+  const int src_lane = (t & 28) | ((0x8D >> (2 * q)) & 3);   // quad exchange: 0 <- 1, 1 <- 3, 2 <- 0, 3 <- 2
+  Reducer8 R{red, 0};
+  auto slot = [&](int row, int half) { return (row * 2 + half) * HP; };
+
+  // meanwhile: right-hand side, ||gamma||^2 and the violation of the current iterate (sqp.py:111-115)
+  const double* gamw = P.gammaw + (size_t)b * vlen + hk * NX + hh * HN;
+  double lam[HN], r[HN], p[HN];
+#pragma unroll
+  for (int i = 0; i < HN; ++i) {
+    lam[i] = 0.0;
+    p[i] = 0.0;
+    r[i] = hold ? gamw[i] : 0.0;
+  }
+  double g2 = 0.0, viol_part = 0.0;
+  {
+    const double* gam = P.gamma + (size_t)b * vlen;
+    for (int i = t; i < vlen; i += blockDim.x) g2 = fma(gam[i], gam[i], g2);
+    const double* eb = P.e + (size_t)b * N * NX;
+    for (int i = t; i < N * NX; i += blockDim.x) viol_part += fabs(eb[i]);
+    const double* xs = P.x_start + (size_t)b * NX;
+    const double* x0 = P.X + (size_t)b * nb * NX;
+    if (t < NX) viol_part += fabs(xs[t] - x0[t]);
+  }
+  const double lbw = hold ? P.lbw[(size_t)b * nb + hk] : 0.0;
+  mbar_wait0(bar);
+
+  // ---- one-time: O^_k = W_k L_k^-T in place, one row per thread and round ----
+  for (int idx = t; idx < N * NX; idx += blockDim.x) {
+    double* row = Wm + (size_t)(idx / NX) * L::BSP + (idx % NX) * NX;
+    const double* Lp = LiG + (size_t)(idx / NX) * L::TRP;
+    double x[NX], o[NX];
+    vec_load<NX>(row, x);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int l = 0; l <= j; ++l) {
+        const double m = Lp[j * (j + 1) / 2 + l];
+        if (l & 1) a1 = fma(x[l], m, a1);
+        else a0 = fma(x[l], m, a0);
+      }
+      o[j] = a0 + a1;
+    }
+    vec_store<NX>(row, o);
+  }
+  __syncthreads();
+  // The lanes that keep a half of u_k (0 and 3) store their quadrant transposed and swap the roles of the
+  // two input halves, so that in every lane the FIRST accumulator set is the one to send and the SECOND
+  // the one to keep -- no per-lane selects around the exchange.
+  double Q[HN][HN];
+  {
+    const double* Ok = Wm + (size_t)k * L::BSP + (qa * HN) * NX + qc * HN;
+#pragma unroll
+    for (int i = 0; i < HN; ++i)
+#pragma unroll
+      for (int j = 0; j < HN; ++j) Q[i][j] = has_blk ? (isw ? Ok[i * NX + j] : Ok[j * NX + i]) : 0.0;
+  }
+  const int in_first = isw ? slot(k, qc) : slot(k + 1, qa);    // multiplies along the rows of Q
+  const int in_second = isw ? slot(k + 1, qa) : slot(k, qc);   // ... along its columns
+
+  auto dot = [&](const double* x, const double* y) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int i = 0; i + 1 < HN; i += 2) {
+      a0 = fma(x[i], y[i], a0);
+      a1 = fma(x[i + 1], y[i + 1], a1);
+    }
+    if constexpr (HN & 1) a0 = fma(x[HN - 1], y[HN - 1], a0);
+    return a0 + a1;
+  };
+  auto load_half = [&](const double* src, double* v) {   // HN doubles from a 16-byte aligned slot
+#pragma unroll
+    for (int j = 0; j < (HN + 1) / 2; ++j) {
+      const double2 c = reinterpret_cast<const double2*>(src)[j];
+      v[2 * j] = c.x;
+      if (2 * j + 1 < HN) v[2 * j + 1] = c.y;
+    }
+  };
+  auto store_half = [&](double* dst, const double* v) {
+#pragma unroll
+    for (int j = 0; j < (HN + 1) / 2; ++j)
+      reinterpret_cast<double2*>(dst)[j] = make_double2(v[2 * j], (2 * j + 1 < HN) ? v[2 * j + 1] : 0.0);
+  };
+  auto publish = [&](const double* v) {
+    if (hold) store_half(xv + slot(hk, hh), v);
+  };
+  // after the barrier that follows publish(v): keep = this lane's half of u_k (lanes 0, 3) or w_k (lanes 1, 2);
+  // the halves of u_k go to shared memory for the owners of row k+1
+  auto products = [&](double* keep) {
+    double v1[HN], v2[HN], snd[HN];
+    load_half(xv + in_first, v1);
+    load_half(xv + in_second, v2);
+#pragma unroll
+    for (int i = 0; i < HN; ++i) {
+      snd[i] = 0.0;
+      keep[i] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < HN; ++i)
+#pragma unroll
+      for (int j = 0; j < HN; ++j) {
+        snd[i] = fma(Q[i][j], v1[j], snd[i]);     // lanes 1, 2: partial u_k;  lanes 0, 3: partial w_k
+        keep[j] = fma(Q[i][j], v2[i], keep[j]);   // lanes 1, 2: partial w_k;  lanes 0, 3: partial u_k
+      }
+#pragma unroll
+    for (int i = 0; i < HN; ++i) keep[i] += __shfl_sync(0xffffffffu, snd[i], src_lane);
+    if (!isw && has_blk) store_half(xu + slot(k + 1, qa), keep);
+  };
+  // after the barrier that follows products(): this lane's half of O^ v
+  auto total = [&](const double* keep, double* tot) {
+    double lo[HN];
+#pragma unroll
+    for (int i = 0; i < HN; ++i) lo[i] = 0.0;
+    if (isw && has_blk && k > 0) load_half(xu + slot(k, hh), lo);
+#pragma unroll
+    for (int i = 0; i < HN; ++i) tot[i] = keep[i] + lo[i];
+  };
+  // sum_rows ((L v)_row)^2 for the vector in slot layout, rows dealt round-robin (the few exact-norm iterations)
+  auto tri_rows_norm2 = [&](const double* vec) {
+    double n2 = 0.0;
+    for (int idx = t; idx < vlen; idx += blockDim.x) {
+      const int kr = idx / NX, i = idx % NX;
+      const double* Lr = LfS + (size_t)kr * L::TRP + i * (i + 1) / 2;
+      const double* v0 = vec + slot(kr, 0);
+      double sacc = 0.0;
+      for (int j = 0; j <= i; ++j) sacc = fma(Lr[j], v0[j < HN ? j : j - HN + HP], sacc);
+      n2 = fma(sacc, sacc, n2);
+    }
+    return n2;
+  };
+
+  int its = 0, breakdown = 0;
+  bool nan_curv = false, verify = false, exact = false;
+  const double2 s = R.sum2(g2, viol_part);
+  const double viol = s.y;
+  const double tol2 = P.pcg_tol * P.pcg_tol;
+  if (!(sqrt(s.x) <= P.pcg_tol)) {   // blocktri.py:146-148
+    double w[HN], tot[HN];
+    publish(r);
+    __syncthreads();
+    products(w);
+    double rz = R.sum1(hold ? dot(r, r) - (isw ? 2.0 * dot(r, w) : 0.0) : 0.0);   // r^ . (I - O^) r^
+    total(w, tot);
+#pragma unroll
+    for (int i = 0; i < HN; ++i) p[i] = r[i] - tot[i];   // z^ = (I - O^) r^
+    const int cap = P.pcg_cap;
+    for (int it = 1; it <= cap; ++it) {
+      publish(p);
+      __syncthreads();
+      products(w);
+      const double curv = R.sum1(hold ? dot(p, p) + (isw ? 2.0 * dot(p, w) : 0.0) : 0.0);   // p^ . (I + O^) p^
+      if (curv <= 0.0) {  // blocktri.py:158-161
+        breakdown = it;
+        break;
+      }
+      if (curv != curv) {  // NaN never satisfies a comparison: the reference runs to the cap
+        nan_curv = true;
+        its = cap;
+        break;
+      }
+      total(w, tot);
+      const double a = rz / curv;
+#pragma unroll
+      for (int i = 0; i < HN; ++i) {
+        lam[i] = lam[i] + a * p[i];
+        r[i] = r[i] - a * (p[i] + tot[i]);   // q^ = (I + O^) p^
+      }
+      publish(r);
+      __syncthreads();
+      products(w);
+      const double rr_own = hold ? dot(r, r) : 0.0;
+      double n2 = lbw * rr_own;   // lower bound of this half row's share of ||L_k r^_k||^2
+      if (exact) n2 = tri_rows_norm2(xv);
+      double2 rr = R.sum2(rr_own - ((hold && isw) ? 2.0 * dot(r, w) : 0.0), n2);
+      total(w, tot);
+      its = it;
+      if (!exact && rr.y <= tol2) {   // the bound no longer excludes convergence: exact norm from now on
+        exact = true;
+        rr.y = R.sum1(tri_rows_norm2(xv));
+      }
+      if (verify || rr.y <= tol2) {
+        // true residual L (gamma^ - lam^ - O^ lam^) of blocktri.py:165
+        double d[HN], dt[HN];
+        publish(lam);
+        __syncthreads();
+        products(d);
+        __syncthreads();
+        total(d, dt);
+#pragma unroll
+        for (int i = 0; i < HN; ++i) dt[i] = hold ? gamw[i] - lam[i] - dt[i] : 0.0;
+        publish(dt);
+        __syncthreads();
+        const double true2 = R.sum1(tri_rows_norm2(xv));
+        if (sqrt(true2) <= P.pcg_tol) break;
+        verify = true;
+      }
+      const double beta = rr.x / rz;
+#pragma unroll
+      for (int i = 0; i < HN; ++i) p[i] = (r[i] - tot[i]) + beta * p[i];   // z^ + beta p^
+      rz = rr.x;
+    }
+  }
+
+  if (breakdown) {
+    if (t == 0) pcg_on_breakdown(P, b, si, breakdown);
+    return;
+  }
+
+  // ---- lambda = L^-T lam^, then recover_step (qpform.py:375-397), rows dealt as in k_pcg_rt ----
+  __syncthreads();          // the O^ blocks are dead: their shared memory now carries three vectors
+  double* vp = mats;               // lambda
+  double* vr = vp + vlen + 2;      // q - lambda
+  double* vw = vr + vlen + 2;      // lam^, later grad_u
+  if (hold) {
+#pragma unroll
+    for (int i = 0; i < HN; ++i) vw[hk * NX + hh * HN + i] = nan_curv ? nan("") : lam[i];
+  }
+  __syncthreads();
+  const int nrows = nb * HN;
+  for (int idx = t; idx < nrows; idx += blockDim.x) {
+    const int kr = idx / HN, i0 = idx % HN, i1 = i0 + HN, kk = kr * NX;
+    const double* g = P.grad + ((size_t)b * nb + kr) * (NX + NU);
+    const double* Lp = LiG + (size_t)kr * L::TRP;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+      const double v = vw[kk + l];
+      const double m0 = (l >= i0) ? Lp[l * (l + 1) / 2 + i0] : 0.0;
+      const double m1 = (l >= i1) ? Lp[l * (l + 1) / 2 + (l >= i1 ? i1 : 0)] : 0.0;
+      a0 = fma(m0, v, a0);
+      a1 = fma(m1, v, a1);
+    }
+    vp[kk + i0] = a0;
+    vp[kk + i1] = a1;
+    P.lam[(size_t)b * vlen + kk + i0] = a0;
+    P.lam[(size_t)b * vlen + kk + i1] = a1;
+    vr[kk + i0] = g[i0] - a0;
+    vr[kk + i1] = g[i1] - a1;
+  }
+  __syncthreads();
+  double* vu = vw;  // grad_u  [N][NU]   (vw's lam^ is dead after the barrier above)
+  const double* hinv = P.hinv + (size_t)b * HS;
+  for (int idx = t; idx < N * HN; idx += blockDim.x) {
+    const int kr = idx / HN, i0 = idx % HN;
+    const double* g = P.grad + ((size_t)b * nb + kr) * (NX + NU);
+    const double* Bk = P.B + ((size_t)b * N + kr) * NX * NU;
+    const double* ln = vp + (kr + 1) * NX;
+    for (int ju = i0; ju < NU; ju += HN) {
+      double su = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) su = fma(Bk[j * NU + ju], ln[j], su);
+      vu[kr * NU + ju] = g[NX + ju] + su;
+    }
+  }
+  __syncthreads();
+  double step_part = 0.0;
+  for (int idx = t; idx < nrows; idx += blockDim.x) {
+    const int kr = idx / HN, i0 = idx % HN, i1 = i0 + HN, kk = kr * NX;
+    const double* Qk = (kr < N) ? hinv : hinv + BS;
+    const double* gk = vr + kk;
+    double d0 = -dot_row<NX>(Qk + i0 * NX, gk);
+    double d1 = -dot_row<NX>(Qk + i1 * NX, gk);
+    if (kr < N) {   // -Q^-1 A_k^T lam_{k+1} = phi_k^T lam_{k+1}
+      const double* Ph = P.Soff + ((size_t)b * N + kr) * BS;
+      const double* ln = vp + (kr + 1) * NX;
+      double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        e0 = fma(Ph[j * NX + i0], ln[j], e0);
+        e1 = fma(Ph[j * NX + i1], ln[j], e1);
+      }
+      d0 += e0;
+      d1 += e1;
+    }
+    double* dX = P.dX + ((size_t)b * nb + kr) * NX;
+    dX[i0] = d0;
+    dX[i1] = d1;
+    step_part = nanmax(step_part, nanmax(fabs(d0), fabs(d1)));
+    if (kr < N) {
+      const double* Ri = hinv + 2 * BS;
+      const double* gu = vu + kr * NU;
+      double* dU = P.dU + ((size_t)b * N + kr) * NU;
+      for (int ju = i0; ju < NU; ju += HN) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
+        dU[ju] = -acc;
+        step_part = nanmax(step_part, fabs(acc));
+      }
     }
   }
   const double step_inf = R.max1(step_part);

@@ -233,10 +233,11 @@ def test_random_instances_over_the_model_pool_match_the_oracle(seed):
     assert np.max(np.abs(got[:upto, 5] - want[:upto, 5])) <= 1
 
 
-@pytest.mark.parametrize("M,N", [(1, 1), (3, 2), (5, 3), (7, 35), (2, 36), (1, 255), (33, 5)])
+@pytest.mark.parametrize("M,N", [(1, 1), (3, 2), (5, 3), (7, 35), (2, 36), (3, 64), (2, 65), (1, 255), (33, 5)])
 def test_boundary_horizons_match_the_compiled_oracle(M, N):
-    """Shortest horizons, the last horizon of the register-resident PCG kernel (N=35), the first of the
-    fat-thread kernel (N=36) and the longest supported one (N+1 = 256 block rows), iiwa14, against the
+    """Shortest horizons, the last horizon of the row-resident PCG kernel (N=35), the first and last of the
+    quadrant-resident kernel (N=36, N=64), the first of the fat-thread kernel (N=65) and the longest
+    supported one (N+1 = 256 block rows), iiwa14, against the
     compiled C oracle: trajectories and per-iteration PCG counts."""
     from oracle import trajopt_c as oc
     from oracle import trajopt_np as orc
@@ -295,3 +296,46 @@ def test_point_masses_in_every_supported_dimension(dims):
     assert len(got) == len(want) == 4
     assert np.max(np.abs(got[:, 5] - want[:, 5])) <= 1
     assert rel_inf(got[:, 1], want[:, 1]) <= 1e-9
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+import paper_2510_07625_b200 as gb
+from paper_2510_07625_b200 import workloads, _lib
+M, N, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+batch = workloads.iiwa14_reach_arrays(M, N, seed=11)
+eng = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, workloads.fixed_budget_settings(3))
+try:
+    res = eng.solve(batch)
+finally:
+    eng.close()
+np.savez(out, X=res.X, U=res.U, pcg=res.trace[:, :, _lib.TRACE_PCG_ITERATIONS], alpha=res.trace[:, :, _lib.TRACE_ALPHA],
+         status=res.info[:, _lib.INFO_STATUS])
+"""
+
+
+@pytest.mark.parametrize("N", [8, 32])
+def test_pcg_kernel_variants_agree(N, tmp_path):
+    """The three PCG kernels (rows of O^ in registers; quadrants of O^ in registers; one thread per block
+    row with O^ in shared memory) are selected by horizon; the GATO_PCG_* switches are read once per
+    process, so each variant solves the same batch in its own interpreter.  Same whitened recurrence,
+    different summation orders: trajectories to 1e-9, PCG counts within one, identical step lengths."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for name, env in (("rt", {}), ("quad", {"GATO_PCG_Q": "2"}), ("fat", {"GATO_PCG_Q": "0", "GATO_PCG_RT": "0"})):
+        path = str(tmp_path / f"{name}.npz")
+        e = dict(os.environ, **env)
+        e["PYTHONPATH"] = root + os.pathsep + e.get("PYTHONPATH", "")
+        subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, "5", str(N), path], check=True, env=e, cwd=root,
+                       timeout=300)
+        outs.append(np.load(path))
+    base = outs[0]
+    assert np.all(base["status"] == 0)
+    for o in outs[1:]:
+        assert np.all(o["status"] == 0)
+        assert rel_inf(o["X"], base["X"]) <= 1e-9 and rel_inf(o["U"], base["U"]) <= 1e-9
+        assert np.max(np.abs(o["pcg"] - base["pcg"])) <= 1
+        assert np.array_equal(o["alpha"], base["alpha"])
