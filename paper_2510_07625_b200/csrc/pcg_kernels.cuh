@@ -1024,15 +1024,41 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
 #pragma unroll
     for (int i = 0; i < HN; ++i) tot[i] = keep[i] + lo[i];
   };
-  // sum_rows ((L v)_row)^2 for the vector in slot layout, rows dealt round-robin (the few exact-norm iterations)
+  // ||L v||^2 for the vector in slot layout (the few exact-norm iterations): lane (a, c) of quad k forms
+  // the rows a-half of L_k[:, c-half] v_k[c-half] (full block below the diagonal, triangle on it, nothing
+  // above), one shuffle joins the two column halves; block row N has no quad and goes to the first threads.
   auto tri_rows_norm2 = [&](const double* vec) {
     double n2 = 0.0;
-    for (int idx = t; idx < vlen; idx += blockDim.x) {
-      const int kr = idx / NX, i = idx % NX;
-      const double* Lr = LfS + (size_t)kr * L::TRP + i * (i + 1) / 2;
-      const double* v0 = vec + slot(kr, 0);
+    {
+      double vc[HN], srow[HN];
+      load_half(vec + slot(k, qc), vc);
+      const double* Lr = LfS + (size_t)k * L::TRP;
+#pragma unroll
+      for (int i = 0; i < HN; ++i) {
+        const int row = qa * HN + i;
+        const double* Li = Lr + row * (row + 1) / 2 + qc * HN;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < HN; ++j) {
+          const bool use = (qa > qc) || (qa == qc && j <= i);
+          const double m = use ? Li[j] : 0.0;
+          if (j & 1) a1 = fma(m, vc[j], a1);
+          else a0 = fma(m, vc[j], a0);
+        }
+        srow[i] = a0 + a1;
+      }
+#pragma unroll
+      for (int i = 0; i < HN; ++i) srow[i] += __shfl_xor_sync(0xffffffffu, srow[i], 1);
+      if (has_blk && qc == 0) {
+#pragma unroll
+        for (int i = 0; i < HN; ++i) n2 = fma(srow[i], srow[i], n2);
+      }
+    }
+    if (t < NX) {
+      const double* Lr = LfS + (size_t)N * L::TRP + t * (t + 1) / 2;
+      const double* v0 = vec + slot(N, 0);
       double sacc = 0.0;
-      for (int j = 0; j <= i; ++j) sacc = fma(Lr[j], v0[j < HN ? j : j - HN + HP], sacc);
+      for (int j = 0; j <= t; ++j) sacc = fma(Lr[j], v0[j < HN ? j : j - HN + HP], sacc);
       n2 = fma(sacc, sacc, n2);
     }
     return n2;
@@ -1049,6 +1075,7 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     __syncthreads();
     products(w);
     double rz = R.sum1(hold ? dot(r, r) - (isw ? 2.0 * dot(r, w) : 0.0) : 0.0);   // r^ . (I - O^) r^
+    double inv_rz = 1.0 / rz;   // formed while the products run
     total(w, tot);
 #pragma unroll
     for (int i = 0; i < HN; ++i) p[i] = r[i] - tot[i];   // z^ = (I - O^) r^
@@ -1103,10 +1130,11 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
         if (sqrt(true2) <= P.pcg_tol) break;
         verify = true;
       }
-      const double beta = rr.x / rz;
+      const double beta = rr.x * inv_rz;
 #pragma unroll
       for (int i = 0; i < HN; ++i) p[i] = (r[i] - tot[i]) + beta * p[i];   // z^ + beta p^
       rz = rr.x;
+      inv_rz = 1.0 / rz;
     }
   }
 
