@@ -435,9 +435,9 @@ def run_gpu_arm(args, w, rank, local_rank, world):
         fam_ms = {"linearize": kern_ms["linearize"], "schur": kern_ms["schur"] + kern_ms["hessinv"],
                   "pcg": kern_ms["pcg"], "linesearch": kern_ms["linesearch"]}
         dominant = max(fam_ms, key=fam_ms.get)
-        # the PCG family (model_ops.cuh: launch_pcg): rows of O^ in registers at short horizons, quadrants of
-        # O^ in registers up to N = 64, one thread per block row above
-        pcg_kernel = "k_pcg_rt" if (N + 1) * 7 <= 256 else "k_pcg_q" if N <= 64 else "k_pcg"
+        # the PCG family (model_ops.cuh: launch_pcg): quadrants of O^ in registers up to N = 64, one thread
+        # per block row above
+        pcg_kernel = "k_pcg_q" if N <= 64 else "k_pcg"
         kernel_names = {"linearize": "k_lin_tangent_iiwa", "schur": "k_schur", "pcg": pcg_kernel,
                         "linesearch": "k_linesearch"}
         launches_dom = K_sqp

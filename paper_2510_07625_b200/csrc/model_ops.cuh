@@ -86,12 +86,14 @@ bool pcg_use_rt(int N) {
          pcg_rt_smem_bytes<Mdl::NX>(N) <= kMaxSmem;
 }
 
-// quad variant (one quadrant of O^_k per thread, in registers) for horizons up to 64; GATO_PCG_Q=0 disables,
-// GATO_PCG_Q=2 prefers it over the real-time variant as well
+// quad variant (one quadrant of O^_k per thread, in registers) for horizons up to 64.  Measured on B200 it
+// also beats the row-resident variant where both apply (M=32, N=32: 0.0983 vs 0.1004 ms; M=1: 0.500 vs
+// 0.527 ms), so it is the default there too: GATO_PCG_Q=1 restricts it to the horizons k_pcg_rt cannot
+// take, GATO_PCG_Q=0 disables it
 template <class Mdl>
 int pcg_use_q(int N) {
   static int mode = -1;
-  if (mode < 0) mode = env_int("GATO_PCG_Q", 1);
+  if (mode < 0) mode = env_int("GATO_PCG_Q", 2);
   if (Mdl::NX < 14 || N < 1 || pcg_q_threads(N) > kPcgQMaxThreads || pcg_q_smem_bytes<Mdl::NX>(N) > kMaxSmem) return 0;
   return mode;
 }

@@ -325,7 +325,7 @@ def test_pcg_kernel_variants_agree(N, tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for name, env in (("rt", {}), ("quad", {"GATO_PCG_Q": "2"}), ("fat", {"GATO_PCG_Q": "0", "GATO_PCG_RT": "0"})):
+    for name, env in (("quad", {"GATO_PCG_Q": "2"}), ("rt", {"GATO_PCG_Q": "1"}), ("fat", {"GATO_PCG_Q": "0", "GATO_PCG_RT": "0"})):
         path = str(tmp_path / f"{name}.npz")
         e = dict(os.environ, **env)
         e["PYTHONPATH"] = root + os.pathsep + e.get("PYTHONPATH", "")
