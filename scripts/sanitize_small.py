@@ -16,9 +16,10 @@ import paper_2510_07625_b200 as gb  # noqa: E402
 from paper_2510_07625_b200 import workloads  # noqa: E402
 from conftest import load_golden, product_problem, product_settings  # noqa: E402
 
-# iiwa14: real-time PCG (N=8), fat-thread PCG with O^ and L resident (N=40 > 35), O^ resident only
-# (N=100), everything in global memory (N=150); the control-step call, best-of-batch, hypothesis selection
-for N, iters in ((8, 2), (40, 1), (100, 1), (150, 1)):
+# iiwa14: quadrant PCG (N=8, N=40, N=64 = the full CTA; with GATO_PCG_Q=1 in the environment N=8 runs the
+# row-resident k_pcg_rt instead), fat-thread PCG with O^ and L resident (N=70), O^ resident only (N=100),
+# everything in global memory (N=150); the control-step call, best-of-batch, hypothesis selection
+for N, iters in ((8, 2), (40, 1), (64, 1), (70, 1), (100, 1), (150, 1)):
     batch = workloads.iiwa14_reach_arrays(3, N)
     eng = gb.BatchEngine(gb.Iiwa14(), 3, N, 0.02, workloads.fixed_budget_settings(iters), loop_mode=3)
     res = eng.solve(batch)
