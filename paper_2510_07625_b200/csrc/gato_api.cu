@@ -231,6 +231,7 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   P.C = cfg->num_shrinks + 1;
   P.regularize_r = cfg->regularize_r;
   P.retry_limit = cfg->pcg_retry_limit;
+  P.dense_schur = env_int("GATO_SCHUR_DENSE", 0);
   P.h = cfg->timestep;
   P.pcg_tol = cfg->pcg_tolerance;
   P.mu = cfg->mu;

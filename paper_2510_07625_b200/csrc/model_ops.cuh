@@ -68,9 +68,10 @@ cudaError_t launch_linearize(const RowView& V, const ModelParams& mp, double h, 
   return cudaGetLastError();
 }
 
+constexpr int kSchurWarps = 2;
 template <class Mdl>
 cudaError_t launch_schur(const SolveParams& P, cudaStream_t s) {
-  constexpr int WARPS = 4;
+  constexpr int WARPS = kSchurWarps;
   const size_t smem = WARPS * sizeof(SchurSmem<Mdl::NX, Mdl::NU>);
   const int64_t warps = (int64_t)P.M * (P.N + 1);
   k_schur<Mdl::NX, Mdl::NU, WARPS><<<(unsigned)((warps + WARPS - 1) / WARPS), WARPS * 32, smem, s>>>(P);
@@ -211,8 +212,8 @@ cudaError_t prepare_attrs(const SolveParams& P) {
                                (int)linp::smem_bytes());
     if (err != cudaSuccess) return err;
   }
-  err = cudaFuncSetAttribute(k_schur<NX, NU, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(4 * sizeof(SchurSmem<NX, NU>)));
+  err = cudaFuncSetAttribute(k_schur<NX, NU, kSchurWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kSchurWarps * sizeof(SchurSmem<NX, NU>)));
   if (err != cudaSuccess) return err;
   {
     const PcgShape sh = pcg_shape<Mdl>(P.N, P.M);

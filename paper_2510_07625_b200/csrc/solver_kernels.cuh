@@ -31,7 +31,7 @@ enum {
 };
 
 struct SolveParams {
-  int M, N, max_it, pcg_cap, C, regularize_r, retry_limit, pad0;
+  int M, N, max_it, pcg_cap, C, regularize_r, retry_limit, dense_schur;   // dense_schur: GATO_SCHUR_DENSE=1, no diagonal-weight shortcut
   double h, pcg_tol, mu, rho_min, rho_max, rho_factor, step_tol, feas_tol;
   ModelParams mp;
   // caller buffers
@@ -739,7 +739,7 @@ struct SchurSmem {
 };
 
 template <int NX, int NU, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 3) k_schur(SolveParams P) {
+__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_schur(SolveParams P) {
   extern __shared__ __align__(16) double schur_smem_raw[];
   using L = PcgLayout<NX>;
   constexpr int HALF = NX / 2;
@@ -868,31 +868,60 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_schur(SolveParams P) {
         if (idx < NU * NU) S.R[idx] = vr[i];
       }
     }
+    // Diagonal weights (the usual tracking cost) leave (Q + rho I)^-1 and (R + rho I)^-1 exactly diagonal
+    // (Cholesky, solve and symmetrisation of a diagonal matrix only ever add exact zeros); with finite A, B
+    // the dense products below then reduce to one multiplication per entry with the same rounding, so the
+    // shortcut changes no result bit (signed zeros aside).  Anything else takes the dense path.
+    bool qdiag = !P.dense_schur, rdiag = !P.dense_schur;
+#pragma unroll
+    for (int i = 0; i < RA; ++i) {
+      const int idx = lane + 32 * i;
+      if (idx < NX * NX) qdiag = qdiag && (idx / NX == idx % NX || vq[i] == 0.0) && isfinite(va[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) rdiag = rdiag && isfinite(vb[i]);
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+      const int idx = lane + 32 * i;
+      if (idx < NU * NU) rdiag = rdiag && (idx / NU == idx % NU || vr[i] == 0.0);
+    }
+    qdiag = __all_sync(0xffffffffu, qdiag);
+    rdiag = __all_sync(0xffffffffu, rdiag);
     __syncwarp();
     const int r = lane >> 1, c0 = (lane & 1) * HALF;
     const bool strip = lane < 2 * NX;
     if (strip) {   // AQ[r][c0 .. c0+HALF) = A[r][:] Q^-1[:, c0 ..]
       double acc[HALF];
+      if (qdiag) {
 #pragma unroll
-      for (int i = 0; i < HALF; ++i) acc[i] = 0.0;
+        for (int i = 0; i < HALF; ++i) acc[i] = S.A[r * NX + c0 + i] * S.Q[(c0 + i) * (NX + 1)];
+      } else {
 #pragma unroll
-      for (int l = 0; l < NX; ++l) {
-        const double a = S.A[r * NX + l];
+        for (int i = 0; i < HALF; ++i) acc[i] = 0.0;
 #pragma unroll
-        for (int i = 0; i < HALF; ++i) acc[i] = fma(a, S.Q[l * NX + c0 + i], acc[i]);
+        for (int l = 0; l < NX; ++l) {
+          const double a = S.A[r * NX + l];
+#pragma unroll
+          for (int i = 0; i < HALF; ++i) acc[i] = fma(a, S.Q[l * NX + c0 + i], acc[i]);
+        }
       }
 #pragma unroll
       for (int i = 0; i < HALF; ++i) S.AQ[r * NX + c0 + i] = acc[i];
     }
     if (lane < NX) {   // BR[lane][:] = B[lane][:] R^-1
       double acc[NU];
+      if (rdiag) {
 #pragma unroll
-      for (int i = 0; i < NU; ++i) acc[i] = 0.0;
+        for (int i = 0; i < NU; ++i) acc[i] = S.B[lane * NU + i] * S.R[i * (NU + 1)];
+      } else {
 #pragma unroll
-      for (int l = 0; l < NU; ++l) {
-        const double bv = S.B[lane * NU + l];
+        for (int i = 0; i < NU; ++i) acc[i] = 0.0;
 #pragma unroll
-        for (int i = 0; i < NU; ++i) acc[i] = fma(bv, S.R[l * NU + i], acc[i]);
+        for (int l = 0; l < NU; ++l) {
+          const double bv = S.B[lane * NU + l];
+#pragma unroll
+          for (int i = 0; i < NU; ++i) acc[i] = fma(bv, S.R[l * NU + i], acc[i]);
+        }
       }
 #pragma unroll
       for (int i = 0; i < NU; ++i) S.BR[lane * NU + i] = acc[i];

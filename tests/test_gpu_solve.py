@@ -339,3 +339,23 @@ def test_pcg_kernel_variants_agree(N, tmp_path):
         assert rel_inf(o["X"], base["X"]) <= 1e-9 and rel_inf(o["U"], base["U"]) <= 1e-9
         assert np.max(np.abs(o["pcg"] - base["pcg"])) <= 1
         assert np.array_equal(o["alpha"], base["alpha"])
+
+
+def test_diagonal_weight_shortcut_is_bitwise_the_dense_schur_products(tmp_path):
+    """k_schur multiplies by the diagonal of (Q + rho I)^-1 and (R + rho I)^-1 when these are exactly
+    diagonal; GATO_SCHUR_DENSE=1 (read once per process) forces the dense products.  Same bits."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for name, env in (("shortcut", {"GATO_SCHUR_DENSE": "0"}), ("dense", {"GATO_SCHUR_DENSE": "1"})):
+        path = str(tmp_path / f"{name}.npz")
+        e = dict(os.environ, **env)
+        e["PYTHONPATH"] = root + os.pathsep + e.get("PYTHONPATH", "")
+        subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, "6", "24", path], check=True, env=e, cwd=root, timeout=300)
+        outs.append(np.load(path))
+    a, c = outs
+    assert np.all(a["status"] == 0)
+    for key in ("X", "U", "pcg", "alpha"):
+        assert np.array_equal(a[key], c[key]), key
