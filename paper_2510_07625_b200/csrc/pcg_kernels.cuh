@@ -854,6 +854,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_pcg(SolveParams P) {
 // the packed L_k for the few exact-norm iterations (see k_pcg) and, before the loop, the record.
 // Half-vectors sit in slots of HP = 10 doubles so the 16-byte loads of a quarter-warp hit distinct banks.
 // -----------------------------------------------------------------------------------------
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
 constexpr int kPcgQMaxThreads = 256;
 __host__ __device__ constexpr int pcg_q_hp(int NX) { return ((NX / 2 + 1) & ~1) + 2; }
 // (a full CTA for short horizons, its spare warps sharing the one-time row loops, was measured: slower --
@@ -933,26 +937,48 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
   const double lbw = hold ? P.lbw[(size_t)b * nb + hk] : 0.0;
   mbar_wait0(bar);
 
-  // ---- one-time: O^_k = W_k L_k^-T in place, one row per thread and round ----
-  for (int idx = t; idx < N * NX; idx += blockDim.x) {
-    double* row = Wm + (size_t)(idx / NX) * L::BSP + (idx % NX) * NX;
-    const double* Lp = LiG + (size_t)(idx / NX) * L::TRP;
-    double x[NX], o[NX];
-    vec_load<NX>(row, x);
+  // ---- one-time: O^_k = W_k L_k^-T in place.  The four lanes of quad k take rows q, q+4, q+8, q+12 of
+  // their own block, so only the warp has to synchronise before the quadrants are read.  L_k^-1 comes
+  // straight from global memory ONCE per lane, in three column groups that fit the registers; the
+  // groups run from the last columns to the first because column j only needs the original W[:, 0..j].
+  auto whiten_cols = [&](auto j0c, auto j1c) {
+    constexpr int J0 = decltype(j0c)::value, J1 = decltype(j1c)::value;
+    constexpr int E0 = J0 * (J0 + 1) / 2, CNT = J1 * (J1 + 1) / 2 - E0;
+    double Lr[CNT];
+    const double* Lp = LiG + (size_t)k * L::TRP + E0;
 #pragma unroll
-    for (int j = 0; j < NX; ++j) {
-      double a0 = 0.0, a1 = 0.0;
+    for (int e = 0; e < CNT; ++e) Lr[e] = has_blk ? Lp[e] : 0.0;
 #pragma unroll
-      for (int l = 0; l <= j; ++l) {
-        const double m = Lp[j * (j + 1) / 2 + l];
-        if (l & 1) a1 = fma(x[l], m, a1);
-        else a0 = fma(x[l], m, a0);
+    for (int rr = 0; rr < (NX + 3) / 4; ++rr) {
+      const int rw = q + 4 * rr;
+      if (has_blk && rw < NX) {
+        double* row = Wm + (size_t)k * L::BSP + rw * NX;
+        double x[J1], o[J1 - J0];
+#pragma unroll
+        for (int l = 0; l < J1; ++l) x[l] = row[l];
+#pragma unroll
+        for (int j = J0; j < J1; ++j) {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int l = 0; l <= j; ++l) {
+            const double m = Lr[j * (j + 1) / 2 - E0 + l];
+            if (l & 1) a1 = fma(x[l], m, a1);
+            else a0 = fma(x[l], m, a0);
+          }
+          o[j - J0] = a0 + a1;
+        }
+#pragma unroll
+        for (int j = J0; j < J1; ++j) row[j] = o[j - J0];
       }
-      o[j] = a0 + a1;
     }
-    vec_store<NX>(row, o);
+  };
+  {
+    constexpr int JA = (NX * 4 + 6) / 7, JB = (NX * 11 + 13) / 14;   // n = 14: columns 0-7 | 8-10 | 11-13
+    whiten_cols(IntC<JB>{}, IntC<NX>{});
+    whiten_cols(IntC<JA>{}, IntC<JB>{});
+    whiten_cols(IntC<0>{}, IntC<JA>{});
   }
-  __syncthreads();
+  __syncwarp();
   // The lanes that keep a half of u_k (0 and 3) store their quadrant transposed and swap the roles of the
   // two input halves, so that in every lane the FIRST accumulator set is the one to send and the SECOND
   // the one to keep -- no per-lane selects around the exchange.
