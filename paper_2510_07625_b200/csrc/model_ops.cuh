@@ -95,7 +95,7 @@ template <class Mdl>
 int pcg_use_q(int N) {
   static int mode = -1;
   if (mode < 0) mode = env_int("GATO_PCG_Q", 2);
-  if (Mdl::NX < 14 || N < 1 || pcg_q_threads(N) > kPcgQMaxThreads || pcg_q_smem_bytes<Mdl::NX>(N) > kMaxSmem) return 0;
+  if (Mdl::NX < 14 || Mdl::NU > Mdl::NX / 2 || N < 1 || pcg_q_threads(N) > kPcgQMaxThreads || pcg_q_smem_bytes<Mdl::NX>(N) > kMaxSmem) return 0;
   return mode;
 }
 

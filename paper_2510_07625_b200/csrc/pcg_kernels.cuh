@@ -1169,7 +1169,37 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     return;
   }
 
-  // ---- lambda = L^-T lam^, then recover_step (qpform.py:375-397), rows dealt as in k_pcg_rt ----
+  // ---- lambda = L^-T lam^, then recover_step (qpform.py:375-397), rows dealt as in k_pcg_rt: item
+  // (block row, i) forms rows i and i + n/2.  7 (N + 1) items never exceed two per thread, and the three
+  // barrier-separated phases would each expose one L2 round trip per item; instead both items of a thread
+  // go together and every global operand is requested one phase ahead (L_k^-1, the gradient and B_k before
+  // lam^ is even published, phi_k and R^-1 while B_k is consumed).
+  static_assert(NU <= HN, "one control row per item");
+  const int nrows = nb * HN;
+  int e_kr[2], e_i0[2];
+  bool e_ok[2];
+  double m0[2][NX], m1[2][HN], gx0[2], gx1[2], gu0[2], bcol[2][NX];
+#pragma unroll
+  for (int rd = 0; rd < 2; ++rd) {
+    const int idx = t + rd * (int)blockDim.x;
+    e_ok[rd] = idx < nrows;
+    e_kr[rd] = e_ok[rd] ? idx / HN : 0;
+    e_i0[rd] = e_ok[rd] ? idx % HN : 0;
+    const int kr = e_kr[rd], i0 = e_i0[rd], i1 = i0 + HN;
+    const double* g = P.grad + ((size_t)b * nb + kr) * (NX + NU);
+    const double* Lp = LiG + (size_t)kr * L::TRP;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) m0[rd][l] = (l >= i0) ? Lp[l * (l + 1) / 2 + i0] : 0.0;
+#pragma unroll
+    for (int l = HN; l < NX; ++l) m1[rd][l - HN] = (l >= i1) ? Lp[l * (l + 1) / 2 + i1] : 0.0;
+    gx0[rd] = g[i0];
+    gx1[rd] = g[i1];
+    const bool knot = kr < N;
+    const double* Bk = P.B + ((size_t)b * N + (knot ? kr : 0)) * NX * NU;
+    gu0[rd] = (knot && i0 < NU) ? g[NX + i0] : 0.0;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) bcol[rd][j] = (knot && i0 < NU) ? Bk[j * NU + i0] : 0.0;
+  }
   __syncthreads();          // the O^ blocks are dead: their shared memory now carries three vectors
   double* vp = mats;               // lambda
   double* vr = vp + vlen + 2;      // q - lambda
@@ -1179,58 +1209,68 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     for (int i = 0; i < HN; ++i) vw[hk * NX + hh * HN + i] = nan_curv ? nan("") : lam[i];
   }
   __syncthreads();
-  const int nrows = nb * HN;
-  for (int idx = t; idx < nrows; idx += blockDim.x) {
-    const int kr = idx / HN, i0 = idx % HN, i1 = i0 + HN, kk = kr * NX;
-    const double* g = P.grad + ((size_t)b * nb + kr) * (NX + NU);
-    const double* Lp = LiG + (size_t)kr * L::TRP;
+#pragma unroll
+  for (int rd = 0; rd < 2; ++rd) {
+    if (!e_ok[rd]) continue;
+    const int i0 = e_i0[rd], i1 = i0 + HN, kk = e_kr[rd] * NX;
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-    for (int l = 0; l < NX; ++l) {
-      const double v = vw[kk + l];
-      const double m0 = (l >= i0) ? Lp[l * (l + 1) / 2 + i0] : 0.0;
-      const double m1 = (l >= i1) ? Lp[l * (l + 1) / 2 + (l >= i1 ? i1 : 0)] : 0.0;
-      a0 = fma(m0, v, a0);
-      a1 = fma(m1, v, a1);
-    }
+    for (int l = 0; l < NX; ++l) a0 = fma(m0[rd][l], vw[kk + l], a0);
+#pragma unroll
+    for (int l = HN; l < NX; ++l) a1 = fma(m1[rd][l - HN], vw[kk + l], a1);
     vp[kk + i0] = a0;
     vp[kk + i1] = a1;
     P.lam[(size_t)b * vlen + kk + i0] = a0;
     P.lam[(size_t)b * vlen + kk + i1] = a1;
-    vr[kk + i0] = g[i0] - a0;
-    vr[kk + i1] = g[i1] - a1;
+    vr[kk + i0] = gx0[rd] - a0;
+    vr[kk + i1] = gx1[rd] - a1;
+  }
+  // requested now, used after the next two barriers: columns i, i + n/2 of phi_k and row i of R^-1
+  const double* hinv = P.hinv + (size_t)b * HS;
+  double s0[2][NX], s1[2][NX], ri[2][NU];
+#pragma unroll
+  for (int rd = 0; rd < 2; ++rd) {
+    const int kr = e_kr[rd], i0 = e_i0[rd], i1 = i0 + HN;
+    const bool knot = e_ok[rd] && kr < N;
+    const double* Ph = P.Soff + ((size_t)b * N + (knot ? kr : 0)) * BS;
+    const double* Ri = hinv + 2 * BS;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      s0[rd][j] = knot ? Ph[j * NX + i0] : 0.0;
+      s1[rd][j] = knot ? Ph[j * NX + i1] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < NU; ++j) ri[rd][j] = (knot && i0 < NU) ? Ri[i0 * NU + j] : 0.0;
   }
   __syncthreads();
   double* vu = vw;  // grad_u  [N][NU]   (vw's lam^ is dead after the barrier above)
-  const double* hinv = P.hinv + (size_t)b * HS;
-  for (int idx = t; idx < N * HN; idx += blockDim.x) {
-    const int kr = idx / HN, i0 = idx % HN;
-    const double* g = P.grad + ((size_t)b * nb + kr) * (NX + NU);
-    const double* Bk = P.B + ((size_t)b * N + kr) * NX * NU;
-    const double* ln = vp + (kr + 1) * NX;
-    for (int ju = i0; ju < NU; ju += HN) {
-      double su = 0.0;
 #pragma unroll
-      for (int j = 0; j < NX; ++j) su = fma(Bk[j * NU + ju], ln[j], su);
-      vu[kr * NU + ju] = g[NX + ju] + su;
-    }
+  for (int rd = 0; rd < 2; ++rd) {
+    const int kr = e_kr[rd], i0 = e_i0[rd];
+    if (!(e_ok[rd] && kr < N && i0 < NU)) continue;
+    const double* ln = vp + (kr + 1) * NX;
+    double su = 0.0;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) su = fma(bcol[rd][j], ln[j], su);
+    vu[kr * NU + i0] = gu0[rd] + su;
   }
   __syncthreads();
   double step_part = 0.0;
-  for (int idx = t; idx < nrows; idx += blockDim.x) {
-    const int kr = idx / HN, i0 = idx % HN, i1 = i0 + HN, kk = kr * NX;
+#pragma unroll
+  for (int rd = 0; rd < 2; ++rd) {
+    if (!e_ok[rd]) continue;
+    const int kr = e_kr[rd], i0 = e_i0[rd], i1 = i0 + HN, kk = kr * NX;
     const double* Qk = (kr < N) ? hinv : hinv + BS;
     const double* gk = vr + kk;
     double d0 = -dot_row<NX>(Qk + i0 * NX, gk);
     double d1 = -dot_row<NX>(Qk + i1 * NX, gk);
     if (kr < N) {   // -Q^-1 A_k^T lam_{k+1} = phi_k^T lam_{k+1}
-      const double* Ph = P.Soff + ((size_t)b * N + kr) * BS;
       const double* ln = vp + (kr + 1) * NX;
       double e0 = 0.0, e1 = 0.0;
 #pragma unroll
       for (int j = 0; j < NX; ++j) {
-        e0 = fma(Ph[j * NX + i0], ln[j], e0);
-        e1 = fma(Ph[j * NX + i1], ln[j], e1);
+        e0 = fma(s0[rd][j], ln[j], e0);
+        e1 = fma(s1[rd][j], ln[j], e1);
       }
       d0 += e0;
       d1 += e1;
@@ -1239,17 +1279,13 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     dX[i0] = d0;
     dX[i1] = d1;
     step_part = nanmax(step_part, nanmax(fabs(d0), fabs(d1)));
-    if (kr < N) {
-      const double* Ri = hinv + 2 * BS;
+    if (kr < N && i0 < NU) {
       const double* gu = vu + kr * NU;
-      double* dU = P.dU + ((size_t)b * N + kr) * NU;
-      for (int ju = i0; ju < NU; ju += HN) {
-        double acc = 0.0;
+      double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < NU; ++j) acc = fma(Ri[ju * NU + j], gu[j], acc);
-        dU[ju] = -acc;
-        step_part = nanmax(step_part, fabs(acc));
-      }
+      for (int j = 0; j < NU; ++j) acc = fma(ri[rd][j], gu[j], acc);
+      P.dU[((size_t)b * N + kr) * NU + i0] = -acc;
+      step_part = nanmax(step_part, fabs(acc));
     }
   }
   const double step_inf = R.max1(step_part);
