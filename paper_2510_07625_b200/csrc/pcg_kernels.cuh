@@ -935,19 +935,22 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     if (t < NX) viol_part += fabs(xs[t] - x0[t]);
   }
   const double lbw = hold ? P.lbw[(size_t)b * nb + hk] : 0.0;
-  mbar_wait0(bar);
 
   // ---- one-time: O^_k = W_k L_k^-T in place.  The four lanes of quad k take rows q, q+4, q+8, q+12 of
   // their own block, so only the warp has to synchronise before the quadrants are read.  L_k^-1 comes
   // straight from global memory ONCE per lane, in three column groups that fit the registers; the
   // groups run from the last columns to the first because column j only needs the original W[:, 0..j].
-  auto whiten_cols = [&](auto j0c, auto j1c) {
+  // The first two groups are requested before the wait for the record, the third while the first is applied.
+  auto load_cols = [&](auto j0c, auto j1c, double* Lr) {
     constexpr int J0 = decltype(j0c)::value, J1 = decltype(j1c)::value;
     constexpr int E0 = J0 * (J0 + 1) / 2, CNT = J1 * (J1 + 1) / 2 - E0;
-    double Lr[CNT];
     const double* Lp = LiG + (size_t)k * L::TRP + E0;
 #pragma unroll
     for (int e = 0; e < CNT; ++e) Lr[e] = has_blk ? Lp[e] : 0.0;
+  };
+  auto whiten_cols = [&](auto j0c, auto j1c, const double* Lr) {
+    constexpr int J0 = decltype(j0c)::value, J1 = decltype(j1c)::value;
+    constexpr int E0 = J0 * (J0 + 1) / 2;
 #pragma unroll
     for (int rr = 0; rr < (NX + 3) / 4; ++rr) {
       const int rw = q + 4 * rr;
@@ -974,9 +977,15 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
   };
   {
     constexpr int JA = (NX * 4 + 6) / 7, JB = (NX * 11 + 13) / 14;   // n = 14: columns 0-7 | 8-10 | 11-13
-    whiten_cols(IntC<JB>{}, IntC<NX>{});
-    whiten_cols(IntC<JA>{}, IntC<JB>{});
-    whiten_cols(IntC<0>{}, IntC<JA>{});
+    constexpr int TRI = NX * (NX + 1) / 2, EA = JA * (JA + 1) / 2, EB = JB * (JB + 1) / 2;
+    double LC[TRI - EB], LB[EB - EA], LA[EA];
+    load_cols(IntC<JB>{}, IntC<NX>{}, LC);
+    load_cols(IntC<JA>{}, IntC<JB>{}, LB);
+    mbar_wait0(bar);
+    whiten_cols(IntC<JB>{}, IntC<NX>{}, LC);
+    load_cols(IntC<0>{}, IntC<JA>{}, LA);
+    whiten_cols(IntC<JA>{}, IntC<JB>{}, LB);
+    whiten_cols(IntC<0>{}, IntC<JA>{}, LA);
   }
   __syncwarp();
   // The lanes that keep a half of u_k (0 and 3) store their quadrant transposed and swap the roles of the
