@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import dataclasses
 import time
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -134,8 +135,9 @@ def render_error(info_row) -> str | None:
     aux = int(info_row[_lib.INFO_FAIL_AUX])
     if status == _lib.STATUS_FACTORIZATION:
         label = _BLOCK_LABEL[int(info_row[_lib.INFO_FAIL_BLOCK])].format(k=int(info_row[_lib.INFO_FAIL_KNOT]))
+        # the tail is scipy.linalg.cho_factor's LinAlgError text, which the reference embeds (qpform.py:264-266)
         return (f"FactorizationError: SQP iteration {it}: {label} is not positive definite: "
-                f"leading minor of order {aux} is not positive")
+                f"{aux}-th leading minor of the array is not positive definite")
     retries = int(info_row[_lib.INFO_RETRIES])
     return (f"PcgBreakdownError: SQP iteration {it}: PCG broke down {retries} times "
             f"(last at inner iteration {aux})")
@@ -169,19 +171,30 @@ def unpack_results(res: PackedResult):
 # device buffers and the instantiated CUDA graph
 # ------------------------------------------------------------------------------------
 
-_ENGINES: dict = {}
+_ENGINES: OrderedDict = OrderedDict()  # key -> BatchEngine, least recently used first
+_ENGINE_CACHE_SIZE = 16
 
 
-def _engine_for(model, M, N, timestep, settings, device) -> BatchEngine:
+def _engine_for(model, M, N, timestep, settings, device, in_use=(), shard: int = 0) -> BatchEngine:
+    """Cached engine of one configuration.  Eviction is least-recently-used and never closes an engine
+    that the running call still has work on (``in_use``); if every cached engine is busy the cache
+    grows for the duration of the call."""
     model_id, params = device_model(model)
-    key = (model_id, tuple(params), M, N, float(timestep), _settings_key(settings), device)
+    # `shard` keeps two shards of one call apart when they land on the same device with the same shape
+    key = (model_id, tuple(params), M, N, float(timestep), _settings_key(settings), device, shard)
     eng = _ENGINES.get(key)
-    if eng is None:
-        if len(_ENGINES) >= 16:
-            _, old = _ENGINES.popitem()
-            old.close()
-        eng = BatchEngine(model, M, N, timestep, settings, device=device)
-        _ENGINES[key] = eng
+    if eng is not None:
+        _ENGINES.move_to_end(key)
+        return eng
+    if len(_ENGINES) >= _ENGINE_CACHE_SIZE:
+        busy = {id(e) for e in in_use}
+        for old_key in list(_ENGINES):
+            if len(_ENGINES) < _ENGINE_CACHE_SIZE:
+                break
+            if id(_ENGINES[old_key]) not in busy:
+                _ENGINES.pop(old_key).close()
+    eng = BatchEngine(model, M, N, timestep, settings, device=device)
+    _ENGINES[key] = eng
     return eng
 
 
@@ -189,6 +202,20 @@ def clear_engine_cache():
     while _ENGINES:
         _, eng = _ENGINES.popitem()
         eng.close()
+
+
+def _check_problem(p, init) -> None:
+    """Everything pack_problems would trip over for ONE problem, raised as the exception the reference's
+    sqp_solve would raise for it (sqp.py:222-225, qpform.py:113-123), so that batch_solve can isolate the
+    slot (batch.py:92-99) instead of losing the batch."""
+    N, n, m = p.horizon, p.model.state_dim, p.model.control_dim
+    X0 = np.asarray(init[0], dtype=float)
+    U0 = np.asarray(init[1], dtype=float)
+    if X0.size != (N + 1) * n:
+        raise ValueError(f"cannot reshape array of size {X0.size} into shape ({N + 1},{n})")
+    if U0.size != N * m:
+        raise ValueError(f"cannot reshape array of size {U0.size} into shape ({N},{m})")
+    _force_rows(p)
 
 
 def shard_bounds(M: int, shards: int) -> list[tuple[int, int]]:
@@ -215,15 +242,25 @@ def batch_solve(spec, workers: int = 1, devices: list[int] | None = None) -> Bat
     device_ms = 0.0
     pending = []
     for idx in groups.values():
+        good = []
+        for i in idx:   # a problem that cannot be packed fails alone (batch.py:92-99)
+            try:
+                _check_problem(spec.problems[i], spec.inits[i])
+                good.append(i)
+            except Exception as exc:  # noqa: BLE001 - isolate the failing slot
+                errors[i] = f"{type(exc).__name__}: {exc}"
+        idx = good
+        if not idx:
+            continue
         problems = [spec.problems[i] for i in idx]
         packed = pack_problems(problems, [spec.inits[i] for i in idx],
                                [settings[i].rho_init for i in idx])
         devs = devices if devices else [None]
-        for (lo, hi), dev in zip(shard_bounds(len(idx), len(devs)), devs):
+        for shard, ((lo, hi), dev) in enumerate(zip(shard_bounds(len(idx), len(devs)), devs)):
             if hi == lo:
                 continue
             eng = _engine_for(problems[0].model, hi - lo, problems[0].horizon, problems[0].timestep,
-                              settings[idx[0]], dev)
+                              settings[idx[0]], dev, in_use=[e for e, _ in pending], shard=shard)
             eng.upload(packed.slice(lo, hi))
             eng.launch()
             pending.append((eng, idx[lo:hi]))

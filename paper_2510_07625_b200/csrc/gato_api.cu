@@ -64,10 +64,27 @@ struct gato_handle {
   cudaStream_t side = nullptr;             // k_hessinv branch
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t launches = 0;
+  int device = 0;               // the device gato_create ran on: every entry point switches to it
   void* lin_scratch = nullptr;  // model-private linearisation scratch (iiwa14: per-stage link data)
 };
 
 namespace {
+
+// A handle belongs to the device that was current in gato_create; its streams, events, graphs and
+// scratch live there.  Every entry point makes that device current for the duration of the call, so a
+// caller that drives several GPUs from one thread (batch_solve(devices=[...])) needs no device
+// bookkeeping of its own.
+struct DeviceGuard {
+  int prev = -1;
+  bool switched = false;
+  explicit DeviceGuard(const gato_handle* h) {
+    if (!h) return;
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != h->device) switched = cudaSetDevice(h->device) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (switched) cudaSetDevice(prev);
+  }
+};
 
 void set_error(gato_handle* h, const std::string& msg) {
   if (h) h->error = msg;
@@ -138,41 +155,65 @@ void destroy_graph(gato_handle* h) {
   h->graph_valid = false;
 }
 
+// A failed call between cudaStreamBeginCapture and cudaStreamEndCapture must not leave the stream in
+// capture mode: the fallback (unrolled graph, then plain launches) runs on the same stream.
+void abort_capture(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(s, &junk);
+    if (junk) cudaGraphDestroy(junk);
+  }
+  cudaGetLastError();
+}
+
+#define CKC(call)                                                                              \
+  do {                                                                                         \
+    cudaError_t err__ = (call);                                                                \
+    if (err__ != cudaSuccess) {                                                                \
+      set_error(h, std::string(#call) + ": " + cudaGetErrorString(err__));                     \
+      abort_capture(s);                                                                        \
+      destroy_graph(h);                                                                        \
+      return GATO_E_CUDA;                                                                      \
+    }                                                                                          \
+  } while (0)
+
 // prologue -> WHILE(any solve active) { pass }
 int build_while_graph(gato_handle* h, cudaStream_t s) {
   destroy_graph(h);
   CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int rc = enqueue_prologue(h, s);
   if (rc != GATO_OK) {
-    cudaGraph_t junk = nullptr;
-    cudaStreamEndCapture(s, &junk);
-    if (junk) cudaGraphDestroy(junk);
+    abort_capture(s);
     return rc;
   }
   cudaStreamCaptureStatus status;
   cudaGraph_t g = nullptr;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
-  CK(cudaStreamGetCaptureInfo_v2(s, &status, nullptr, &g, &deps, &ndeps));
-  CK(cudaGraphConditionalHandleCreate(&h->cond, g, 1, cudaGraphCondAssignDefault));
+  CKC(cudaStreamGetCaptureInfo_v2(s, &status, nullptr, &g, &deps, &ndeps));
+  CKC(cudaGraphConditionalHandleCreate(&h->cond, g, 1, cudaGraphCondAssignDefault));
   cudaGraphNodeParams np = {};
   np.type = cudaGraphNodeTypeConditional;
   np.conditional.handle = h->cond;
   np.conditional.type = cudaGraphCondTypeWhile;
   np.conditional.size = 1;
   cudaGraphNode_t node;
-  CK(cudaGraphAddNode(&node, g, deps, ndeps, &np));
+  CKC(cudaGraphAddNode(&node, g, deps, ndeps, &np));
   cudaGraph_t body = np.conditional.phGraph_out[0];
-  CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
-  CK(cudaStreamEndCapture(s, &h->graph));
+  CKC(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  CKC(cudaStreamEndCapture(s, &h->graph));
   // body
-  CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  CKC(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   rc = enqueue_pass(h, s, 1);
+  if (rc != GATO_OK) {
+    abort_capture(s);
+    destroy_graph(h);
+    return rc;
+  }
   cudaGraph_t body_out = nullptr;
-  cudaError_t e2 = cudaStreamEndCapture(s, &body_out);
-  if (rc != GATO_OK) return rc;
-  CK(e2);
-  CK(cudaGraphInstantiate(&h->exec, h->graph, 0));
+  CKC(cudaStreamEndCapture(s, &body_out));
+  CKC(cudaGraphInstantiate(&h->exec, h->graph, 0));
   h->graph_valid = true;
   return GATO_OK;
 }
@@ -182,10 +223,12 @@ int build_unrolled_graph(gato_handle* h, cudaStream_t s) {
   CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int rc = enqueue_prologue(h, s);
   for (int it = 0; rc == GATO_OK && it < h->P.max_it; ++it) rc = enqueue_pass(h, s, 0);
-  cudaError_t e2 = cudaStreamEndCapture(s, &h->graph);
-  if (rc != GATO_OK) return rc;
-  CK(e2);
-  CK(cudaGraphInstantiate(&h->exec, h->graph, 0));
+  if (rc != GATO_OK) {
+    abort_capture(s);
+    return rc;
+  }
+  CKC(cudaStreamEndCapture(s, &h->graph));
+  CKC(cudaGraphInstantiate(&h->exec, h->graph, 0));
   h->graph_valid = true;
   return GATO_OK;
 }
@@ -202,6 +245,7 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   if (cfg->abi_version != GATO_ABI_VERSION) return GATO_E_INVALID;
   gato_handle* h = new gato_handle();
   h->cfg = *cfg;
+  if (cudaGetDevice(&h->device) != cudaSuccess) h->device = 0;
   *out = h;  // returned even on failure so that gato_last_error is readable; caller destroys
   if (!select_ops(cfg->model_id, cfg->model_params, &h->ops)) {
     set_error(h, "unknown model id or unsupported model dimension");
@@ -321,6 +365,7 @@ int gato_bind(gato_handle* h, const gato_buffers* b) {
 }
 
 int gato_solve(gato_handle* h, void* stream) {
+  DeviceGuard guard__(h);
   if (!h) return GATO_E_INVALID;
   if (!h->bound) {
     set_error(h, "gato_solve before gato_bind");
@@ -364,6 +409,7 @@ int gato_solve(gato_handle* h, void* stream) {
 /* number of solves still active after the last enqueued pass (synchronises the stream).
  * Non-zero only in loop modes 2/3 when a PCG-breakdown retry consumed a pass. */
 int gato_pending(gato_handle* h, void* stream, int32_t* pending) {
+  DeviceGuard guard__(h);
   if (!h || !pending) return GATO_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CK(cudaStreamSynchronize(s));
@@ -375,6 +421,7 @@ int gato_pending(gato_handle* h, void* stream, int32_t* pending) {
 
 /* enqueue `passes` further SQP passes without re-initialising (loop modes 2/3 after retries) */
 int gato_resume(gato_handle* h, void* stream, int32_t passes) {
+  DeviceGuard guard__(h);
   if (!h || !h->bound) return GATO_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int it = 0; it < passes; ++it) {
@@ -385,6 +432,7 @@ int gato_resume(gato_handle* h, void* stream, int32_t passes) {
 }
 
 int gato_shift_warm_start(gato_handle* h, void* stream) {
+  DeviceGuard guard__(h);
   if (!h || !h->bound) return GATO_E_INVALID;
   const SolveParams& P = h->P;
   const size_t bytes = ((size_t)(P.N + 1) * h->ops.nx + (size_t)P.N * h->ops.nu) * sizeof(double);
@@ -398,6 +446,7 @@ int gato_shift_warm_start(gato_handle* h, void* stream) {
 
 int gato_mpc_advance(gato_handle* h, void* stream, const double* goal_path, int64_t path_len, int64_t path_stride,
                      int64_t step) {
+  DeviceGuard guard__(h);
   if (!h || !h->bound) return GATO_E_INVALID;
   if (goal_path && (path_len < 1 || step < 0 || path_stride < 0)) {
     set_error(h, "gato_mpc_advance: path_len >= 1, step >= 0, path_stride >= 0");
@@ -417,6 +466,7 @@ int gato_mpc_advance(gato_handle* h, void* stream, const double* goal_path, int6
 }
 
 int gato_merit_candidates(gato_handle* h, void* stream, const double* dX, const double* dU) {
+  DeviceGuard guard__(h);
   if (!h || !h->bound) return GATO_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const SolveParams& P = h->P;
@@ -432,6 +482,7 @@ int gato_merit_candidates(gato_handle* h, void* stream, const double* dX, const 
 }
 
 int gato_best_of_batch(gato_handle* h, void* stream, int32_t* best_index, double* best_merit) {
+  DeviceGuard guard__(h);
   if (!h || !h->bound) return GATO_E_INVALID;
   k_best_of_batch<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(h->P, best_index, best_merit);
   CK(cudaGetLastError());
@@ -440,6 +491,7 @@ int gato_best_of_batch(gato_handle* h, void* stream, int32_t* best_index, double
 
 int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host_in, int64_t in_bytes,
                     int32_t shift_first, const void* dev_out, void* host_out, int64_t out_bytes) {
+  DeviceGuard guard__(h);
   if (!h) return GATO_E_INVALID;
   if (!h->bound) {
     set_error(h, "gato_solve_host before gato_bind");
@@ -486,6 +538,7 @@ int gato_scratch(gato_handle* h, const char* name, void** dev_ptr, int64_t* coun
 }
 
 int gato_read_scratch(gato_handle* h, const char* name, void* host_dst, int64_t bytes) {
+  DeviceGuard guard__(h);
   void* src = nullptr;
   int64_t count = 0;
   int rc = gato_scratch(h, name, &src, &count);
@@ -496,6 +549,7 @@ int gato_read_scratch(gato_handle* h, const char* name, void* host_dst, int64_t 
 }
 
 int64_t gato_launch_count(const gato_handle* h) {
+  DeviceGuard guard__(h);
   if (!h) return 0;
   unsigned int c[4] = {0, 0, 0, 0};
   if (cudaMemcpy(c, h->P.counters, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
@@ -510,6 +564,7 @@ int gato_loop_mode(const gato_handle* h) { return h ? h->loop_mode : 0; }
  * every pass: ms[0..5] = total device time of hessinv, linearize, schur, pcg, linesearch, update
  * over the max_sqp_iterations passes, ms[6] = prologue, ms[7] = whole call. Synchronous. */
 int gato_solve_profiled(gato_handle* h, void* stream, float* ms) {
+  DeviceGuard guard__(h);
   if (!h || !ms) return GATO_E_INVALID;
   if (!h->bound) return GATO_E_UNBOUND;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -572,6 +627,7 @@ int gato_measure_fp64_peak(double* tflops) {
 }
 
 int gato_last_solve_ms(gato_handle* h, float* ms) {
+  DeviceGuard guard__(h);
   if (!h || !ms) return GATO_E_INVALID;
   CK(cudaEventSynchronize(h->ev1));
   CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
@@ -581,6 +637,7 @@ int gato_last_solve_ms(gato_handle* h, float* ms) {
 const char* gato_last_error(const gato_handle* h) { return h ? h->error.c_str() : "null handle"; }
 
 void gato_destroy(gato_handle* h) {
+  DeviceGuard guard__(h);
   if (!h) return;
   destroy_graph(h);
   if (h->ev0) cudaEventDestroy(h->ev0);

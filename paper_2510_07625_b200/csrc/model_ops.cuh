@@ -172,7 +172,7 @@ template <class Mdl>
 cudaError_t launch_linesearch(const SolveParams& P, cudaStream_t s) {
   int threads = ((P.N + 31) / 32) * 32;
   if (threads > 128) threads = 128;
-  dim3 grid(P.C + 1, P.M);   // C step-length candidates + the alpha = 0 candidate of the first iteration
+  dim3 grid(P.M, P.C + 1);   // C step-length candidates + the alpha = 0 candidate of the first iteration
   static int minb = 0;
   if (!minb) minb = env_int("GATO_LS_MINB", 1);
   if (minb == 3) k_linesearch<Mdl, 3><<<grid, threads, 0, s>>>(P);

@@ -33,13 +33,13 @@ namespace gato {
 // ---- shared pieces ------------------------------------------------------------------------
 
 // factorisation failure reported by k_schur for this solve?  (thread 0 records it)
-__device__ __forceinline__ bool pcg_schur_failed(const SolveParams& P, int b, int32_t* si) {
-  if (si[SI_SCHUR_FAIL] == INT_MAX) return false;
-  if (threadIdx.x == 0) {
-    const int key = si[SI_SCHUR_FAIL];
-    si[SI_SCHUR_FAIL] = INT_MAX;
-    record_failure(P, b, GATO_STATUS_FACTORIZATION, key / 64, GATO_BLOCK_S, key % 64, 0);
-  }
+// The word is only written by k_init (reset) and k_schur (atomicMin), never in a PCG kernel, so every
+// thread of the CTA reads the same value and the decision is CTA-uniform; record_failure deactivates the
+// solve, so the word is not looked at again before the next k_init.
+__device__ __forceinline__ bool pcg_schur_failed(const SolveParams& P, int b, const int32_t* si) {
+  const int key = si[SI_SCHUR_FAIL];
+  if (key == INT_MAX) return false;
+  if (threadIdx.x == 0) record_failure(P, b, GATO_STATUS_FACTORIZATION, key / 64, GATO_BLOCK_S, key % 64, 0);
   return true;
 }
 

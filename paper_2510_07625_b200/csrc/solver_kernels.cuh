@@ -1183,15 +1183,15 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
 }
 
 // -----------------------------------------------------------------------------------------
-// k_linesearch: merit of every candidate (sqp.py:132-166).  grid (C, M), one thread per stage
+// k_linesearch: merit of every candidate (sqp.py:132-166).  grid (M, C), one thread per stage
 // knot: candidate point (X + a dX, U + a dU), one RK4 prediction, |defect|_1, quadratic cost
 // with the undamped weights; fixed-tree reduction over knots.  Non-finite candidates -> +inf.
-// grid (C + 1, M): the extra candidate is alpha = 0, evaluated only while merit(X0, U0) is unknown.
+// grid (M, C + 1): the extra candidate is alpha = 0, evaluated only while merit(X0, U0) is unknown.
 // -----------------------------------------------------------------------------------------
 template <class Mdl, int MINB = 1>
 __global__ void __launch_bounds__(128, MINB) k_linesearch(SolveParams P) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU, NF = Mdl::NF;
-  const int c = blockIdx.x, b = blockIdx.y;
+  const int c = blockIdx.y, b = blockIdx.x;   // solves on grid.x: no 65 535 cap on the batch
   const int32_t* si = P.si + b * SI_WORDS;
   const int skip = si[SI_SKIP_LS];
   if (c < P.C) {

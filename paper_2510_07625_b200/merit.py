@@ -6,7 +6,6 @@ bookkeeping."""
 
 from __future__ import annotations
 
-import math
 
 import numpy as np
 
@@ -69,4 +68,3 @@ def adapt_rho(rho: float, accepted: bool, settings: SolverSettings) -> float:
 
 
 __all__ = ["adapt_rho", "constraint_l1", "line_search", "merit", "merit_many"]
-_ = math

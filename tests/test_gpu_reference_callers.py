@@ -1,0 +1,175 @@
+"""The reference's OWN callers on the swapped backend ("unchanged
+callers must work").  `__graft_entry__.build()` installs the unmodified reference package into baseline/_ref
+(git-ignored; it travels to the GPU box with the snapshot).  Here `trajbatch.mpc.batch_solve` -- the name
+`_MpcEngine.advance` calls (mpc.py:274) -- is replaced by the CUDA adapter and the reference's closed loop
+`run_mpc` (mpc.py:361-383: hypothesis sampling, warm-start shift, hypothesis selection, plant simulation, all
+the reference's own code) is run for >= 10 control steps; the applied controls, selected hypotheses and states
+must match the run with the reference's CPU batch_solve.  Same for `trajbatch.batch_solve`'s direct callers
+in pkg/tests/test_batch.py (single = direct, worker counts, failed slot isolated)."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from conftest import rel_inf
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tb():
+    from oracle import ref_bridge
+    mod = ref_bridge.load()
+    if mod is None:
+        pytest.skip("reference package not installed (baseline/_ref); build() installs it in the build container")
+    return mod
+
+
+@pytest.fixture
+def gpu_batch_solve(tb, monkeypatch):
+    """trajbatch.mpc.batch_solve -> the CUDA adapter; yields a call counter."""
+    import paper_2510_07625_b200 as gb
+    import trajbatch.mpc as ref_mpc
+    calls = {"n": 0, "solves": 0}
+
+    def adapter(spec, workers=1):
+        calls["n"] += 1
+        calls["solves"] += spec.size
+        return gb.batch_solve(spec, workers=workers)
+
+    monkeypatch.setattr(ref_mpc, "batch_solve", adapter)
+    yield calls
+    gb.batch.clear_engine_cache()
+
+
+def _arm_problem(tb, N=8, h=0.05):
+    model = tb.TwoLinkArm()
+    goal = np.concatenate([model.inverse_kinematics(np.array([0.6, 0.2])), np.zeros(2)])
+    cost = tb.CostSpec(Q=np.diag([10.0, 10.0, 0.1, 0.1]), R=1e-2 * np.eye(2), QN=np.diag([100.0, 100.0, 1.0, 1.0]),
+                       goal=goal)
+    return tb.ProblemSpec(model=model, cost=cost, horizon=N, timestep=h, x_start=np.array([0.2, 0.3, 0.0, 0.0]))
+
+
+def _compare_traces(cpu, gpu, tol):
+    assert gpu.steps == cpu.steps
+    assert list(gpu.selected) == list(cpu.selected), "a different hypothesis was executed"
+    assert rel_inf(np.asarray(gpu.controls), np.asarray(cpu.controls)) <= tol
+    assert rel_inf(np.asarray(gpu.states), np.asarray(cpu.states)) <= tol
+    assert rel_inf(np.asarray(gpu.merits), np.asarray(cpu.merits)) <= 1e-6
+
+
+def test_run_mpc_hypothesis_mode_two_link_arm(tb, monkeypatch):
+    """pkg/tests/test_mpc.py:155-171 shape: 12 control steps, 6 force hypotheses, true force unknown to the
+    controller.  CPU run first (unpatched), then the same call with the CUDA adapter."""
+    import paper_2510_07625_b200 as gb
+    import trajbatch.mpc as ref_mpc
+    problem = _arm_problem(tb)
+    kw = dict(plant_cfg=tb.PlantConfig(h_plant=0.01), true_disturbance=tb.ExternalForce.constant([2.0, -1.0]),
+              steps=12, mode=tb.HypothesisMode(6, 0.8),
+              settings=tb.SolverSettings(max_sqp_iterations=2, step_tolerance=None), seed=3)
+    cpu = tb.run_mpc(problem, **kw)
+    calls = {"n": 0}
+
+    def adapter(spec, workers=1):
+        calls["n"] += 1
+        return gb.batch_solve(spec, workers=workers)
+
+    monkeypatch.setattr(ref_mpc, "batch_solve", adapter)
+    try:
+        gpu = tb.run_mpc(problem, **kw)
+    finally:
+        gb.batch.clear_engine_cache()
+    assert calls["n"] == 12
+    _compare_traces(cpu, gpu, 1e-6)
+    for t in range(gpu.steps):     # test_mpc.py:169-171 on the swapped backend
+        chosen = gpu.hypothesis_forces[t][gpu.selected[t]]
+        np.testing.assert_array_equal(gpu.centers_after[t], chosen)
+
+
+def test_run_mpc_rho_sweep_mode_pendulum(tb, monkeypatch):
+    """mpc.py:250-258, 283-290: per-member warm starts and best-of-batch by final merit (RhoSweepMode)."""
+    import paper_2510_07625_b200 as gb
+    import trajbatch.mpc as ref_mpc
+    cost = tb.CostSpec(Q=np.diag([1.0, 0.1]), R=np.diag([0.01]), QN=np.diag([100.0, 10.0]), goal=np.array([np.pi, 0.0]))
+    problem = tb.ProblemSpec(model=tb.Pendulum(), cost=cost, horizon=16, timestep=0.05, x_start=np.zeros(2))
+    kw = dict(plant_cfg=tb.PlantConfig(h_plant=0.01), true_disturbance=None, steps=10, mode=tb.RhoSweepMode(4),
+              settings=tb.SolverSettings(max_sqp_iterations=5, step_tolerance=None), seed=0)
+    cpu = tb.run_mpc(problem, **kw)
+    monkeypatch.setattr(ref_mpc, "batch_solve", lambda spec, workers=1: gb.batch_solve(spec, workers=workers))
+    try:
+        gpu = tb.run_mpc(problem, **kw)
+    finally:
+        gb.batch.clear_engine_cache()
+    _compare_traces(cpu, gpu, 1e-5)
+    assert np.all(np.isfinite(gpu.merits))
+
+
+def test_mpc_engine_advance_iiwa14(tb, gpu_batch_solve):
+    """_MpcEngine.advance (mpc.py:240-330) with the iiwa14 model plugged into the reference through its
+    DynamicsModel interface: 10 control steps, 4 flange-force hypotheses, 2 SQP iterations per step."""
+    import trajbatch.mpc as ref_mpc
+    from oracle import ref_bridge
+    from paper_2510_07625_b200 import workloads
+    model = ref_bridge.iiwa14_model()
+    Q, R, QN = workloads.iiwa14_cost_weights()
+    q0 = np.array([0.1, -0.3, 0.2, 0.5, -0.1, 0.3, 0.0])
+    goal = np.concatenate([q0 + 0.3, np.zeros(7)])
+    problem = tb.ProblemSpec(model=model, cost=tb.CostSpec(Q, R, QN, goal), horizon=8, timestep=0.02,
+                             x_start=np.concatenate([q0, np.zeros(7)]), force=tb.ExternalForce.zero(3))
+    args = (problem, tb.PlantConfig(h_plant=0.01), tb.ExternalForce.constant([3.0, -2.0, 1.0]),
+            tb.HypothesisMode(4, 5.0), tb.SolverSettings(max_sqp_iterations=2, step_tolerance=None,
+                                                        pcg=tb.PcgSettings(tolerance=1e-6)), 7)
+    gpu_eng = ref_mpc._MpcEngine(*args)
+    for _ in range(10):
+        gpu_eng.advance()
+    assert gpu_batch_solve["n"] == 10 and gpu_batch_solve["solves"] == 40
+    assert not gpu_eng.solver_error_steps
+    # the same engine on the reference's CPU batch_solve
+    import trajbatch.batch as ref_batch
+    import pytest as _pytest
+    mp = _pytest.MonkeyPatch()
+    mp.setattr(ref_mpc, "batch_solve", ref_batch.batch_solve)
+    try:
+        cpu_eng = ref_mpc._MpcEngine(*args)
+        for _ in range(10):
+            cpu_eng.advance()
+    finally:
+        mp.undo()
+    _compare_traces(cpu_eng.trace(), gpu_eng.trace(), 1e-6)
+
+
+def test_reference_batch_tests_on_the_swapped_backend(tb):
+    """pkg/tests/test_batch.py:40-75 with batch_solve / sqp_solve replaced by the CUDA adapter and the
+    reference's own types as inputs: single = direct, `workers` does not change results, a failed slot is
+    isolated with the reference's message."""
+    import paper_2510_07625_b200 as gb
+    cost = tb.CostSpec(Q=np.diag([1.0, 0.1]), R=np.diag([0.01]), QN=np.diag([100.0, 10.0]), goal=np.array([np.pi, 0.0]))
+    problem = tb.ProblemSpec(model=tb.Pendulum(), cost=cost, horizon=16, timestep=0.05, x_start=np.zeros(2))
+    zero = (np.zeros((17, 2)), np.zeros((16, 1)))
+    st = tb.SolverSettings(max_sqp_iterations=8, step_tolerance=None)
+    try:
+        direct = gb.sqp_solve(problem, *zero, st)
+        batch = gb.batch_solve(tb.BatchSpec([problem], [zero], st))
+        assert np.array_equal(direct.X, batch.results[0].X) and np.array_equal(direct.U, batch.results[0].U)
+        ref_direct = tb.sqp_solve(problem, *zero, st)
+        assert rel_inf(direct.X, ref_direct.X) <= 1e-6 and len(direct.trace) == len(ref_direct.trace)
+
+        st6 = tb.SolverSettings(max_sqp_iterations=6, step_tolerance=None)
+        spec = tb.BatchSpec.with_rho_inits([problem] * 8, [zero] * 8, st6, tb.rho_grid(8))
+        serial, parallel = gb.batch_solve(spec, workers=1), gb.batch_solve(spec, workers=2)
+        ref = tb.batch_solve(spec, workers=1)
+        for a, b, r in zip(serial.results, parallel.results, ref.results):
+            assert np.array_equal(a.X, b.X) and np.array_equal(a.U, b.U)
+            assert rel_inf(a.X, r.X) <= 1e-6 and rel_inf(a.U, r.U) <= 1e-6
+            assert [x.rho for x in a.trace] == pytest.approx([x.rho for x in r.trace], rel=1e-12)
+
+        bad_cost = dataclasses.replace(cost, Q=np.diag([-5.0, 0.1]))
+        bad = dataclasses.replace(problem, cost=bad_cost)
+        mixed = tb.BatchSpec([problem, bad, problem], [zero] * 3, st6)
+        got, want = gb.batch_solve(mixed), tb.batch_solve(mixed)
+        assert [e is None for e in got.errors] == [e is None for e in want.errors] == [True, False, True]
+        assert got.errors[1] == want.errors[1], "error text of the failed slot"
+        assert got.results[1] is None and np.array_equal(got.results[0].X, got.results[2].X)
+    finally:
+        gb.batch.clear_engine_cache()

@@ -69,21 +69,21 @@ def test_restart_at_solution_returns_one_record_and_untouched_iterate():
     assert np.array_equal(again.X, g["X"]) and np.array_equal(again.U, g["U"])
 
 
-def test_rejected_iterations_leave_the_iterate_bitwise_unchanged():
-    """test_sqp.py:221-251: with a huge penalty-free direction every step is rejected."""
-    g = load_golden("pendulum_n8")
-    problem = product_problem(g)
-    # start at the converged solution with a fixed budget: steps are ~0 and never strictly decrease
-    sol = load_golden("pendulum_n8_tol")
-    p2 = product_problem(sol)
-    st = dataclasses.replace(product_settings(sol), step_tolerance=None, max_sqp_iterations=4)
-    res = gb.sqp_solve(p2, sol["X"], sol["U"], st)
-    rejected = [r for r in res.trace if not r.accepted]
-    if len(rejected) == len(res.trace):
-        assert np.array_equal(res.X, sol["X"]) and np.array_equal(res.U, sol["U"])
-    merits = [r.merit for r in res.trace]
+@pytest.mark.parametrize("case,idx", [("cartpole_n8", 1), ("cartpole_n8", 3), ("twolink_n8", 5), ("di1_n4", 3)])
+def test_rejected_iterations_leave_the_iterate_bitwise_unchanged(case, idx):
+    """test_sqp.py:221-251: re-run to the boundary on each side of a rejected iteration and compare the
+    iterates exactly.  The golden traces (unmodified reference) say which iterations are rejected; the
+    device must reject the same ones."""
+    g = load_golden(case)
+    assert g["trace"][idx, 6] == 0.0, "fixture: the reference rejected this iteration"
+    problem, st = product_problem(g), product_settings(g)
+    before = gb.sqp_solve(problem, g["X0"], g["U0"], dataclasses.replace(st, max_sqp_iterations=idx))
+    after = gb.sqp_solve(problem, g["X0"], g["U0"], dataclasses.replace(st, max_sqp_iterations=idx + 1))
+    assert len(after.trace) == idx + 1 and not after.trace[idx].accepted
+    assert np.array_equal(before.X, after.X) and np.array_equal(before.U, after.U)
+    assert after.trace[idx].merit == before.trace[idx - 1].merit
+    merits = [r.merit for r in after.trace]
     assert all(b <= a for a, b in zip(merits, merits[1:])), "merit must never increase"
-    assert problem is not None
 
 
 def test_accepted_merits_strictly_decrease_and_trace_is_consistent():

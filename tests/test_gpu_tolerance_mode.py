@@ -1,0 +1,121 @@
+"""Tolerance mode at BASELINE sizes ("also run every config once in tolerance mode,
+defaults sqp.py:56-69, 50 iterations").  configs[1] (batch 32, N = 32) and configs[2] (batch 128, N = 64) with
+the reference's DEFAULT settings -- step tolerance 1e-6, feasibility tolerance 1e-6, PCG tolerance 1e-8, PCG cap
+10 x unknowns, at most 50 SQP iterations -- so that every solve leaves the device-side WHILE loop on its own
+(tolerance exit or budget) while its neighbours keep iterating.
+
+Checked for EVERY solve against the compiled C oracle and for 8 solves against the numpy oracle (bitwise the
+reference): identical record counts and converged flags on >= 95 % of the solves, identical accept / step-length
+sequences up to the first plateau flip, and every flip explained: it happens where the candidate merits are
+indistinguishable at the reference's own rounding sensitivity (the reference flips its accept decision there
+under 1e-13 input perturbations): tiny step, merits equal to 1e-8 relative."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2510_07625_b200 as gb
+from paper_2510_07625_b200 import _lib, workloads
+from conftest import rel_inf
+
+pytestmark = pytest.mark.gpu
+
+PLATEAU_STEP = 1e-3      # |dZ|_inf below which a step counts as a plateau step
+PLATEAU_MERIT = 1e-8     # relative merit difference below which accept / reject is rounding
+
+
+def first_divergence(tg, ng, tc, nc):
+    """Index of the first record whose (alpha, accepted) differ, or None if one trace is the other's prefix
+    and the counts agree.  Rows in the layout of include/gato_b200.h."""
+    for i in range(min(ng, nc)):
+        ag, ac = tg[i, _lib.TRACE_ALPHA], tc[i, _lib.TRACE_ALPHA]
+        same_alpha = (ag == ac) or (np.isnan(ag) and np.isnan(ac))
+        if not same_alpha or tg[i, _lib.TRACE_ACCEPTED] != tc[i, _lib.TRACE_ACCEPTED]:
+            return i
+    return None if ng == nc else min(ng, nc)
+
+
+def on_plateau(tg, tc, i):
+    """Both traces sit on the merit plateau at record i (or one of them has just left the loop there)."""
+    i = min(i, tg.shape[0] - 1, tc.shape[0] - 1)
+    mg, mc = tg[i, _lib.TRACE_MERIT], tc[i, _lib.TRACE_MERIT]
+    sg, sc = tg[i, _lib.TRACE_STEP_INF_NORM], tc[i, _lib.TRACE_STEP_INF_NORM]
+    return abs(mg - mc) <= PLATEAU_MERIT * max(1.0, abs(mc)) and max(sg, sc) <= PLATEAU_STEP
+
+
+def compare(name, got_trace, got_n, got_conv, got_X, got_U, ref_trace, ref_n, ref_conv, ref_X, ref_U, rows):
+    same_count, flips, worst_same, worst_flip = 0, [], 0.0, 0.0
+    for j, b in enumerate(rows):
+        ng, nc = int(got_n[b]), int(ref_n[j])
+        tg, tc = got_trace[b, :ng], ref_trace[j, :nc]
+        same_count += int(ng == nc and bool(got_conv[b]) == bool(ref_conv[j]))
+        err = max(rel_inf(got_X[b], ref_X[j]), rel_inf(got_U[b], ref_U[j]))
+        i = first_divergence(tg, ng, tc, nc)
+        if i is None:
+            worst_same = max(worst_same, err)
+            # identical decisions: PCG counts within +-1 wherever both records exist
+            assert np.max(np.abs(tg[:, _lib.TRACE_PCG_ITERATIONS] - tc[:, _lib.TRACE_PCG_ITERATIONS])) <= 1, (name, b)
+        else:
+            flips.append((b, i))
+            worst_flip = max(worst_flip, err)
+            assert on_plateau(tg, tc, i), f"{name}: solve {b} diverges at iteration {i} off the merit plateau"
+            # up to the flip the two runs are the same run
+            if i > 0:
+                assert rel_inf(tg[:i, _lib.TRACE_MERIT], tc[:i, _lib.TRACE_MERIT]) <= 1e-8, (name, b)
+    return same_count, flips, worst_same, worst_flip
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("M,N,h,kind", [(32, 32, 0.02, "track"), (128, 64, 0.05, "reach")])
+def test_tolerance_mode_at_baseline_sizes(M, N, h, kind):
+    from oracle import trajopt_c as oc
+    from oracle import trajopt_np as orc
+    from oracle.iiwa14_np import Iiwa14
+    batch = workloads.iiwa14_track_arrays(M, N, h) if kind == "track" else workloads.iiwa14_reach_arrays(M, N)
+    st = gb.SolverSettings()                  # the reference's defaults: tolerance mode, 50 iterations
+    assert st.max_sqp_iterations == 50 and st.step_tolerance == 1e-6 and st.pcg.tolerance == 1e-8
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, h, st)
+    try:
+        got = eng.solve(batch)
+        assert eng.loop_mode == 1, "per-solve early exit must run inside the device-side WHILE loop"
+    finally:
+        eng.close()
+    assert np.all(got.info[:, _lib.INFO_STATUS] == 0)
+    n_g, conv_g = got.info[:, _lib.INFO_N_RECORDS], got.info[:, _lib.INFO_CONVERGED]
+    assert n_g.min() >= 1 and n_g.max() <= 50
+
+    ost = orc.Settings()                      # same defaults (sqp.py:56-69)
+    assert ost.max_sqp_iterations == 50 and ost.step_tolerance == 1e-6 and ost.pcg_tolerance == 1e-8
+    X, U, trace, info = oc.solve_batch(batch.x_start, batch.goal, batch.Q, batch.R, batch.QN, batch.force,
+                                       batch.rho_init, batch.X, batch.U, h, ost)
+    assert np.all(info[:, 2] == 0)
+    # C trace rows: same layout as the device's
+    same, flips, worst_same, worst_flip = compare(f"C oracle M={M} N={N}", got.trace, n_g, conv_g, got.X, got.U, trace,
+                                                  info[:, 0], info[:, 1], X, U, range(M))
+    print(f"\n[tolerance mode M={M} N={N}] vs C oracle: identical record count + converged flag on {same}/{M} solves, "
+          f"{len(flips)} plateau flips (first at {sorted(i for _, i in flips)[:5]}), records {n_g.min()}..{n_g.max()}, "
+          f"converged {int(conv_g.sum())}, worst traj err same-decisions {worst_same:.2e}, after a flip {worst_flip:.2e}")
+    assert same >= 0.95 * M, f"record counts differ on {M - same} of {M} solves"
+    assert worst_same <= 1e-4, "north-star tolerance on the solves with identical decisions"
+
+    # the numpy oracle (bitwise the reference) on 8 solves spread over the batch
+    rows = sorted(set(int(r) for r in np.linspace(0, M - 1, 8)))
+    probs = [orc.Problem(Iiwa14(), batch.Q[b], batch.R[b], batch.QN[b], batch.goal[b], N, h, batch.x_start[b],
+                         batch.force[b]) for b in rows]
+    inits = [(batch.X[b], batch.U[b]) for b in rows]
+    res, errors, _ = orc.solve_batch_parallel(probs, inits, [ost] * len(rows), min(len(rows), os.cpu_count() or 1))
+    assert all(e is None for e in errors)
+    width = max(len(r.trace) for r in res)
+    rt = np.full((len(rows), width, 8), np.nan)
+    for j, r in enumerate(res):
+        for rec in r.trace:
+            rt[j, rec.iteration] = [rec.merit, rec.constraint_l1, np.nan if rec.alpha is None else rec.alpha, rec.rho,
+                                    rec.pcg_iterations, float(rec.accepted), rec.step_inf_norm, rec.iteration]
+    same8, flips8, ws8, wf8 = compare(f"numpy oracle M={M} N={N}", got.trace, n_g, conv_g, got.X, got.U, rt,
+                                      [len(r.trace) for r in res], [r.converged for r in res],
+                                      [r.X for r in res], [r.U for r in res], rows)
+    print(f"[tolerance mode M={M} N={N}] vs numpy oracle on solves {rows}: identical count on {same8}/{len(rows)}, "
+          f"{len(flips8)} plateau flips, worst traj err {ws8:.2e} / after a flip {wf8:.2e}")
+    assert same8 >= len(rows) - 1
+    assert ws8 <= 1e-4
