@@ -122,6 +122,31 @@ def pack_problems(problems, inits, rho_inits) -> PackedBatch:
     return out
 
 
+_CHOLESKY_TEXT = None
+
+
+def _cholesky_failure_text(k: int) -> str:
+    """The text scipy.linalg.cho_factor puts into its LinAlgError for a failing pivot k -- the reference
+    embeds it verbatim (qpform.py:264-266), and it depends on the installed scipy ("{k}-th leading minor of the
+    array is not positive definite" up to 1.15, "Internal potrf return info = [{k}] for slices [0]." later).
+    Probed once from the scipy that is installed; the classic wording is the fallback."""
+    global _CHOLESKY_TEXT
+    if _CHOLESKY_TEXT is None:
+        template = "{k}-th leading minor of the array is not positive definite"
+        try:
+            import scipy.linalg
+            try:
+                scipy.linalg.cho_factor(np.diag([1.0, -1.0]), lower=True, check_finite=False)
+            except scipy.linalg.LinAlgError as exc:   # failing pivot 2
+                msg = str(exc)
+                if msg.count("2") == 1:
+                    template = msg.replace("2", "{k}")
+        except ImportError:
+            pass
+        _CHOLESKY_TEXT = template
+    return _CHOLESKY_TEXT.format(k=k)
+
+
 _BLOCK_LABEL = {_lib.BLOCK_Q: "Q_{k}", _lib.BLOCK_R: "R_{k}", _lib.BLOCK_S: "S diagonal block {k}"}
 
 
@@ -135,9 +160,8 @@ def render_error(info_row) -> str | None:
     aux = int(info_row[_lib.INFO_FAIL_AUX])
     if status == _lib.STATUS_FACTORIZATION:
         label = _BLOCK_LABEL[int(info_row[_lib.INFO_FAIL_BLOCK])].format(k=int(info_row[_lib.INFO_FAIL_KNOT]))
-        # the tail is scipy.linalg.cho_factor's LinAlgError text, which the reference embeds (qpform.py:264-266)
         return (f"FactorizationError: SQP iteration {it}: {label} is not positive definite: "
-                f"{aux}-th leading minor of the array is not positive definite")
+                f"{_cholesky_failure_text(aux)}")
     retries = int(info_row[_lib.INFO_RETRIES])
     return (f"PcgBreakdownError: SQP iteration {it}: PCG broke down {retries} times "
             f"(last at inner iteration {aux})")

@@ -51,9 +51,17 @@ def _arm_problem(tb, N=8, h=0.05):
     return tb.ProblemSpec(model=model, cost=cost, horizon=N, timestep=h, x_start=np.array([0.2, 0.3, 0.0, 0.0]))
 
 
-def _compare_traces(cpu, gpu, tol):
+def _compare_traces(cpu, gpu, tol, merit_ties_ok=False):
     assert gpu.steps == cpu.steps
-    assert list(gpu.selected) == list(cpu.selected), "a different hypothesis was executed"
+    if merit_ties_ok:
+        # best-of-batch by final merit (mpc.py:283-290): members that differ only in rho converge to the same
+        # point and their final merits agree to ~1e-9 relative, so the argmin sits on a near-tie that the
+        # rounding of either implementation decides; a different index is accepted only there
+        for t, (a, b) in enumerate(zip(gpu.selected, cpu.selected)):
+            if a != b:
+                assert abs(gpu.merits[t] - cpu.merits[t]) <= 1e-7 * max(1.0, abs(cpu.merits[t])), f"step {t}: not a tie"
+    else:
+        assert list(gpu.selected) == list(cpu.selected), "a different hypothesis was executed"
     assert rel_inf(np.asarray(gpu.controls), np.asarray(cpu.controls)) <= tol
     assert rel_inf(np.asarray(gpu.states), np.asarray(cpu.states)) <= tol
     assert rel_inf(np.asarray(gpu.merits), np.asarray(cpu.merits)) <= 1e-6
@@ -101,7 +109,7 @@ def test_run_mpc_rho_sweep_mode_pendulum(tb, monkeypatch):
         gpu = tb.run_mpc(problem, **kw)
     finally:
         gb.batch.clear_engine_cache()
-    _compare_traces(cpu, gpu, 1e-5)
+    _compare_traces(cpu, gpu, 1e-5, merit_ties_ok=True)
     assert np.all(np.isfinite(gpu.merits))
 
 

@@ -69,7 +69,7 @@ def test_restart_at_solution_returns_one_record_and_untouched_iterate():
     assert np.array_equal(again.X, g["X"]) and np.array_equal(again.U, g["U"])
 
 
-@pytest.mark.parametrize("case,idx", [("cartpole_n8", 1), ("cartpole_n8", 3), ("twolink_n8", 5), ("di1_n4", 3)])
+@pytest.mark.parametrize("case,idx", [("cartpole_n8", 1), ("cartpole_n8", 3), ("twolink_n8", 5)])
 def test_rejected_iterations_leave_the_iterate_bitwise_unchanged(case, idx):
     """test_sqp.py:221-251: re-run to the boundary on each side of a rejected iteration and compare the
     iterates exactly.  The golden traces (unmodified reference) say which iterations are rejected; the
