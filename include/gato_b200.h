@@ -85,6 +85,10 @@ extern "C" {
 #define GATO_TRACE_STEP_INF_NORM 6
 #define GATO_TRACE_ITERATION 7
 
+/* gato_config.flags */
+#define GATO_FLAG_UNFUSED 1 /* keep form_schur in its own kernel and write the plain stage arrays (Sdiag, Soff, Linv,
+                               Lfac, the matrix record) even where the PCG kernel could form the system itself */
+
 typedef struct gato_config {
   int32_t abi_version; /* GATO_ABI_VERSION */
   int32_t model_id;
@@ -100,7 +104,7 @@ typedef struct gato_config {
   int32_t regularize_r;
   int32_t pcg_retry_limit;
   int32_t loop_mode; /* 0 auto, 1 CUDA-graph WHILE node, 2 graph of unrolled passes, 3 plain stream launches */
-  int32_t reserved0;
+  int32_t flags;     /* GATO_FLAG_* */
   double timestep;
   double pcg_tolerance;
   double mu;

@@ -10,6 +10,7 @@ from pathlib import Path
 from .errors import BackendUnavailableError
 
 ABI_VERSION = 1
+FLAG_UNFUSED = 1      # gato_config.flags: keep form_schur in its own kernel, write the plain stage arrays
 INFO_WORDS = 8
 TRACE_WORDS = 8
 (INFO_N_RECORDS, INFO_CONVERGED, INFO_STATUS, INFO_FAIL_ITER, INFO_FAIL_KNOT, INFO_FAIL_BLOCK,
@@ -27,7 +28,7 @@ class GatoConfig(C.Structure):
         ("force_dim", C.c_int32), ("max_sqp_iterations", C.c_int32),
         ("pcg_max_iterations", C.c_int32), ("num_shrinks", C.c_int32),
         ("regularize_r", C.c_int32), ("pcg_retry_limit", C.c_int32), ("loop_mode", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("flags", C.c_int32),
         ("timestep", C.c_double), ("pcg_tolerance", C.c_double), ("mu", C.c_double),
         ("beta", C.c_double), ("rho_min", C.c_double), ("rho_max", C.c_double),
         ("rho_factor", C.c_double), ("step_tolerance", C.c_double),

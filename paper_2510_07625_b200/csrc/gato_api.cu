@@ -276,6 +276,10 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   P.regularize_r = cfg->regularize_r;
   P.retry_limit = cfg->pcg_retry_limit;
   P.dense_schur = env_int("GATO_SCHUR_DENSE", 0);
+  // Schur formation fused into the PCG kernel (schur_quad.cuh) wherever k_pcg_q runs; GATO_FUSED=0, the
+  // config flag GATO_FLAG_UNFUSED or GATO_SCHUR_DENSE=1 keep k_schur + the matrix record (stage arrays for tests)
+  P.fused = (env_int("GATO_FUSED", 1) && !(cfg->flags & GATO_FLAG_UNFUSED) && !P.dense_schur &&
+             h->ops.pcg_fused_ok((int)N)) ? 1 : 0;
   P.h = cfg->timestep;
   P.pcg_tol = cfg->pcg_tolerance;
   P.mu = cfg->mu;

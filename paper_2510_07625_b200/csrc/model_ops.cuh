@@ -25,6 +25,7 @@ struct ModelOps {
   cudaError_t (*select_hypothesis)(const ModelParams&, int, const double*, const double*, const double*,
                                    const double*, double, int, int, double*, int32_t*, cudaStream_t);
   size_t (*pcg_mat_doubles)(int N);            // per-solve padded matrix record (PcgLayout)
+  int (*pcg_fused_ok)(int N);                  // 1: launch_pcg picks k_pcg_q for this horizon, which can form the Schur system itself
   cudaError_t (*prepare)(const SolveParams&);  // opt-in shared memory sizes, outside any capture
 };
 
@@ -204,6 +205,16 @@ size_t pcg_mat_doubles(int N) {
 }
 
 template <class Mdl>
+int pcg_fused_ok(int N) {
+  if constexpr (Mdl::NX >= 14) {
+    const int qmode = pcg_use_q<Mdl>(N);
+    return (qmode == 2 || (qmode == 1 && !pcg_use_rt<Mdl>(N))) ? 1 : 0;
+  } else {
+    return 0;
+  }
+}
+
+template <class Mdl>
 cudaError_t prepare_attrs(const SolveParams& P) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU;
   cudaError_t err;
@@ -245,7 +256,7 @@ ModelOps make_ops() {
   return ModelOps{Mdl::NX,           Mdl::NU,           Mdl::NF,
                   launch_hessinv<Mdl>, launch_linearize<Mdl>, lin_scratch_bytes<Mdl>, launch_schur<Mdl>,
                   launch_pcg<Mdl>,     launch_linesearch<Mdl>, launch_step_rows<Mdl>, launch_select_hypothesis<Mdl>,
-                  pcg_mat_doubles<Mdl>, prepare_attrs<Mdl>};
+                  pcg_mat_doubles<Mdl>, pcg_fused_ok<Mdl>, prepare_attrs<Mdl>};
 }
 
 

@@ -27,6 +27,7 @@
 //             memory when the horizon does not fit), 16-byte row loads, O^_k^T applied by rows.
 #pragma once
 #include "solver_kernels.cuh"
+#include "schur_quad.cuh"
 
 namespace gato {
 
@@ -866,9 +867,13 @@ __host__ __device__ constexpr int pcg_q_threads(int N) { return (4 * N + 31) / 3
 template <int NX>
 __host__ __device__ constexpr size_t pcg_q_smem_bytes(int N) {
   const size_t xch = 2 * (size_t)(N + 1) * 2 * pcg_q_hp(NX) * 8;
-  const size_t mats = ((size_t)N * PcgLayout<NX>::BSP + (size_t)(N + 1) * PcgLayout<NX>::TRP) * 8;
+  // W region (later the packed L_k, later the recovery vectors) + the packed L_k^-1 slots
+  const size_t wreg = (size_t)N * PcgLayout<NX>::BSP > (size_t)(N + 1) * PcgLayout<NX>::TRP
+                          ? (size_t)N * PcgLayout<NX>::BSP : (size_t)(N + 1) * PcgLayout<NX>::TRP;
+  const size_t mats = (wreg + (size_t)(N + 1) * PcgLayout<NX>::TRP) * 8;
   const size_t vecs = 3 * (size_t)((N + 1) * NX + 2) * 8;
-  return 16 * 16 + xch + (mats > vecs ? mats : vecs);
+  const size_t lbw = (size_t)((N + 2) & ~1) * 8;   // stop-test weights of the fused Schur phase
+  return 16 * 16 + xch + lbw + (mats > vecs ? mats : vecs);
 }
 
 template <int NX, int NU>
@@ -888,23 +893,54 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
   double2* red = reinterpret_cast<double2*>(pcg_smem);
   double* xv = reinterpret_cast<double*>(red + 16);   // published vector, slot (row, half) of HP doubles
   double* xu = xv + (size_t)nb * 2 * HP;              // u_k for the owners of row k+1, same slots
-  double* mats = xu + (size_t)nb * 2 * HP;
+  double* lbw_s = xu + (size_t)nb * 2 * HP;           // [nb] stop-test weights (fused Schur phase)
+  double* mats = lbw_s + ((nb + 1) & ~1);
   double* pm = P.pmats + (size_t)b * L::mat_doubles(N);
-  const double* LiG = pm + (size_t)N * L::BSP;          // packed L_k^-1 (global)
-  const double* LfG = LiG + (size_t)nb * L::TRP;        // packed L_k (global)
+  double* LiG = pm + (size_t)N * L::BSP;                // packed L_k^-1 (global)
+  double* LfG = LiG + (size_t)nb * L::TRP;              // packed L_k (global)
   double* Wm = mats;                                    // W_k -> O^_k
-  const double* LfS = mats + (size_t)N * L::BSP;        // packed L_k (shared)
-  __shared__ __align__(8) unsigned long long fill_bar;
+  const size_t wreg = (size_t)N * L::BSP > (size_t)nb * L::TRP ? (size_t)N * L::BSP : (size_t)nb * L::TRP;
+  double* R2 = mats + wreg;                             // packed L_k^-1: slot k = block row k + 1, slot N = block row 0
+  // Fused mode (schur_quad.cuh): this CTA forms the Schur system of its solve itself -- no matrix record, no
+  // k_schur.  CTA-uniform: the flag is written by k_hessinv, two kernels upstream.
+  const bool fused = P.fused && si[SI_DIAG];
+  const double* LfS = mats;   // packed L_k for the exact-norm iterations: bulk-copied over the W region once it is free
+  __shared__ __align__(8) unsigned long long fill_bar, lf_bar_mem;
+  __shared__ QuadDiag<NX, NU> s_diag;
+  __shared__ int s_fail;
   const unsigned bar = (unsigned)__cvta_generic_to_shared(&fill_bar);
-  if (t == 0) mbar_init(bar);
-  if (t < 16) red[t] = make_double2(0.0, 0.0);
-  __syncthreads();
+  const unsigned lf_bar = (unsigned)__cvta_generic_to_shared(&lf_bar_mem);
   if (t == 0) {
-    const unsigned bytes_off = (unsigned)((size_t)N * L::BSP * 8), bytes_tri = (unsigned)((size_t)nb * L::TRP * 8);
-    mbar_expect(bar, bytes_off + bytes_tri);
-    bulk_fill_issue(bar, mats, pm, bytes_off);
-    bulk_fill_issue(bar, mats + (size_t)N * L::BSP, LfG, bytes_tri);
+    mbar_init(bar);
+    mbar_init(lf_bar);
+    s_fail = INT_MAX;
   }
+  if (t < 16) red[t] = make_double2(0.0, 0.0);
+  if (fused) {
+    quad_schur_stage<NX, NU>(P, b, t, N, Wm, R2);   // A_k, B_k on their way into shared memory
+    quad_diag_load<NX, NU>(P, b, t, s_diag);
+  }
+  __syncthreads();
+  if (!fused) {
+    if (t == 0) {
+      const unsigned bytes_off = (unsigned)((size_t)N * L::BSP * 8), bytes_tri = (unsigned)((size_t)nb * L::TRP * 8);
+      mbar_expect(bar, bytes_off + bytes_tri);
+      bulk_fill_issue(bar, mats, pm, bytes_off);
+      bulk_fill_issue(bar, R2, LiG + L::TRP, bytes_tri - (unsigned)(L::TRP * 8));     // block rows 1..N -> slots 0..N-1
+      bulk_fill_issue(bar, R2 + (size_t)N * L::TRP, LiG, (unsigned)(L::TRP * 8));     // block row 0 -> slot N
+    }
+  } else {
+    const QuadSchurIO io{P.A, P.B, P.e, P.X, P.goal, P.U, P.x_start, P.grad, P.gamma, P.gammaw};
+    quad_schur_phase<NX, NU, HP>(io, b, t, N, Wm, R2, xv, xu, lbw_s, &s_fail, s_diag, LfG);
+    asm volatile("fence.proxy.async;" ::: "memory");   // packed L in global memory is bulk-copied back below
+    __syncthreads();
+    if (s_fail != INT_MAX) {   // S block not positive definite (qpform.py:352-353): CTA-uniform exit
+      if (t == 0) record_failure(P, b, GATO_STATUS_FACTORIZATION, s_fail / 64, GATO_BLOCK_S, s_fail % 64, 0);
+      return;
+    }
+  }
+  // packed L_k^-1 of block row kr, in shared memory on both paths
+  auto li_of = [&](int kr) -> const double* { return R2 + (size_t)(kr == 0 ? N : kr - 1) * L::TRP; };
   const int quad = t >> 2, q = t & 3, qa = q >> 1, qc = q & 1;
   const bool has_blk = quad < N;
   const int k = has_blk ? quad : 0;
@@ -934,7 +970,7 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     const double* x0 = P.X + (size_t)b * nb * NX;
     if (t < NX) viol_part += fabs(xs[t] - x0[t]);
   }
-  const double lbw = hold ? P.lbw[(size_t)b * nb + hk] : 0.0;
+  const double lbw = hold ? (fused ? lbw_s[hk] : P.lbw[(size_t)b * nb + hk]) : 0.0;
 
   // ---- one-time: O^_k = W_k L_k^-T in place.  The four lanes of quad k take rows q, q+4, q+8, q+12 of
   // their own block, so only the warp has to synchronise before the quadrants are read.  L_k^-1 comes
@@ -944,7 +980,7 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
   auto load_cols = [&](auto j0c, auto j1c, double* Lr) {
     constexpr int J0 = decltype(j0c)::value, J1 = decltype(j1c)::value;
     constexpr int E0 = J0 * (J0 + 1) / 2, CNT = J1 * (J1 + 1) / 2 - E0;
-    const double* Lp = LiG + (size_t)k * L::TRP + E0;
+    const double* Lp = li_of(k) + E0;
 #pragma unroll
     for (int e = 0; e < CNT; ++e) Lr[e] = has_blk ? Lp[e] : 0.0;
   };
@@ -979,9 +1015,9 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     constexpr int JA = (NX * 4 + 6) / 7, JB = (NX * 11 + 13) / 14;   // n = 14: columns 0-7 | 8-10 | 11-13
     constexpr int TRI = NX * (NX + 1) / 2, EA = JA * (JA + 1) / 2, EB = JB * (JB + 1) / 2;
     double LC[TRI - EB], LB[EB - EA], LA[EA];
+    if (!fused) mbar_wait0(bar);
     load_cols(IntC<JB>{}, IntC<NX>{}, LC);
     load_cols(IntC<JA>{}, IntC<JB>{}, LB);
-    mbar_wait0(bar);
     whiten_cols(IntC<JB>{}, IntC<NX>{}, LC);
     load_cols(IntC<0>{}, IntC<JA>{}, LA);
     whiten_cols(IntC<JA>{}, IntC<JB>{}, LB);
@@ -1104,6 +1140,16 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
   const double2 s = R.sum2(g2, viol_part);
   const double viol = s.y;
   const double tol2 = P.pcg_tol * P.pcg_tol;
+  // every quadrant is in registers (the barrier inside sum2), so the W region is free: the packed L_k (global:
+  // the record, or what the fused Schur phase wrote) come into it with one bulk copy, awaited lazily by the
+  // first exact-norm iteration
+  bool lf_pending = true;
+  if (t == 0) {
+    const unsigned bytes_tri = (unsigned)((size_t)nb * L::TRP * 8);
+    asm volatile("fence.proxy.async;" ::: "memory");
+    mbar_expect(lf_bar, bytes_tri);
+    bulk_fill_issue(lf_bar, mats, LfG, bytes_tri);
+  }
   if (!(sqrt(s.x) <= P.pcg_tol)) {   // blocktri.py:146-148
     double w[HN], tot[HN];
     publish(r);
@@ -1147,6 +1193,10 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
       its = it;
       if (!exact && rr.y <= tol2) {   // the bound no longer excludes convergence: exact norm from now on
         exact = true;
+        if (lf_pending) {
+          mbar_wait0(lf_bar);
+          lf_pending = false;
+        }
         rr.y = R.sum1(tri_rows_norm2(xv));
       }
       if (verify || rr.y <= tol2) {
@@ -1173,6 +1223,8 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     }
   }
 
+  if (lf_pending) mbar_wait0(lf_bar);   // no bulk copy may be in flight when its target is reused or the CTA exits
+
   if (breakdown) {
     if (t == 0) pcg_on_breakdown(P, b, si, breakdown);
     return;
@@ -1196,7 +1248,7 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     e_i0[rd] = e_ok[rd] ? idx % HN : 0;
     const int kr = e_kr[rd], i0 = e_i0[rd], i1 = i0 + HN;
     const double* g = P.grad + ((size_t)b * nb + kr) * (NX + NU);
-    const double* Lp = LiG + (size_t)kr * L::TRP;
+    const double* Lp = li_of(kr);
 #pragma unroll
     for (int l = 0; l < NX; ++l) m0[rd][l] = (l >= i0) ? Lp[l * (l + 1) / 2 + i0] : 0.0;
 #pragma unroll
@@ -1241,12 +1293,15 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
   for (int rd = 0; rd < 2; ++rd) {
     const int kr = e_kr[rd], i0 = e_i0[rd], i1 = i0 + HN;
     const bool knot = e_ok[rd] && kr < N;
-    const double* Ph = P.Soff + ((size_t)b * N + (knot ? kr : 0)) * BS;
+    // phi_k = -A_k Q^-1: k_schur's array, or (fused mode, Q^-1 diagonal) the same products formed here
+    const bool fz = P.fused && si[SI_DIAG];   // = fused, re-read so that it is not live across the iteration
+    const double* Ph = (fz ? P.A : P.Soff) + ((size_t)b * N + (knot ? kr : 0)) * BS;
+    const double sc0 = fz ? -s_diag.qd[i0] : 1.0, sc1 = fz ? -s_diag.qd[i1] : 1.0;
     const double* Ri = hinv + 2 * BS;
 #pragma unroll
     for (int j = 0; j < NX; ++j) {
-      s0[rd][j] = knot ? Ph[j * NX + i0] : 0.0;
-      s1[rd][j] = knot ? Ph[j * NX + i1] : 0.0;
+      s0[rd][j] = knot ? Ph[j * NX + i0] * sc0 : 0.0;
+      s1[rd][j] = knot ? Ph[j * NX + i1] * sc1 : 0.0;
     }
 #pragma unroll
     for (int j = 0; j < NU; ++j) ri[rd][j] = (knot && i0 < NU) ? Ri[i0 * NU + j] : 0.0;

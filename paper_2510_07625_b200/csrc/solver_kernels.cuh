@@ -27,11 +27,13 @@ enum {
   SI_PCG_ITS = 4,
   SI_MERIT_VALID = 5,
   SI_SCHUR_FAIL = 6,
+  SI_DIAG = 7,   // Q, QN, R diagonal (k_hessinv): the solve may take the fused Schur + PCG path
   SI_WORDS = 8
 };
 
 struct SolveParams {
   int M, N, max_it, pcg_cap, C, regularize_r, retry_limit, dense_schur;   // dense_schur: GATO_SCHUR_DENSE=1, no diagonal-weight shortcut
+  int fused;   // 1: solves with diagonal weights form their Schur system inside k_pcg_q (schur_quad.cuh), k_schur skips them
   double h, pcg_tol, mu, rho_min, rho_max, rho_factor, step_tol, feas_tol;
   ModelParams mp;
   // caller buffers
@@ -219,26 +221,52 @@ __global__ void __launch_bounds__(96) k_hessinv(SolveParams P) {
   __shared__ SpdScratch<NX> scr[2];
   __shared__ SpdScratch<NU> scr_u;
   __shared__ int fails[3];
+  __shared__ int offdiag[3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double rho = P.sd[b * SD_WORDS + SD_RHO];
   constexpr int HS = hinv_stride(NX, NU);
   double* out = P.hinv + (size_t)b * HS;
   if (warp < 2) {
     const double* src = (warp == 0 ? P.Q : P.QN) + (size_t)b * NX * NX;
-    for (int idx = lane; idx < NX * NX; idx += 32) W[warp][idx] = src[idx] + ((idx / NX == idx % NX) ? rho : 0.0);
+    int od = 0;   // any non-zero off the diagonal, in the weight or in its damped inverse?
+    for (int idx = lane; idx < NX * NX; idx += 32) {
+      const double v = src[idx];
+      const bool dg = idx / NX == idx % NX;
+      od |= (!dg && v != 0.0) || !isfinite(v);
+      W[warp][idx] = v + (dg ? rho : 0.0);
+    }
     __syncwarp();
     fails[warp] = warp_spd_inverse<NX>(W[warp], scr[warp], lane);
-    for (int idx = lane; idx < NX * NX; idx += 32) out[warp * NX * NX + idx] = W[warp][idx];
+    for (int idx = lane; idx < NX * NX; idx += 32) {
+      const double v = W[warp][idx];
+      od |= (idx / NX != idx % NX && v != 0.0) || !isfinite(v);
+      out[warp * NX * NX + idx] = v;
+    }
+    od = __any_sync(0xffffffffu, od);
+    if (lane == 0) offdiag[warp] = od;
   } else {
     const double* src = P.R + (size_t)b * NU * NU;
     const double rr = P.regularize_r ? rho : 0.0;
-    for (int idx = lane; idx < NU * NU; idx += 32) W[2][idx] = src[idx] + ((idx / NU == idx % NU) ? rr : 0.0);
+    int od = 0;
+    for (int idx = lane; idx < NU * NU; idx += 32) {
+      const double v = src[idx];
+      const bool dg = idx / NU == idx % NU;
+      od |= (!dg && v != 0.0) || !isfinite(v);
+      W[2][idx] = v + (dg ? rr : 0.0);
+    }
     __syncwarp();
     fails[2] = warp_spd_inverse<NU>(W[2], scr_u, lane);
-    for (int idx = lane; idx < NU * NU; idx += 32) out[2 * NX * NX + idx] = W[2][idx];
+    for (int idx = lane; idx < NU * NU; idx += 32) {
+      const double v = W[2][idx];
+      od |= (idx / NU != idx % NU && v != 0.0) || !isfinite(v);
+      out[2 * NX * NX + idx] = v;
+    }
+    od = __any_sync(0xffffffffu, od);
+    if (lane == 0) offdiag[2] = od;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    P.si[b * SI_WORDS + SI_DIAG] = !(offdiag[0] | offdiag[1] | offdiag[2] | fails[0] | fails[1] | fails[2]);
     // reporting order of form_schur: Q_0 .. Q_N first, then R_0 (qpform.py:305-311)
     if (fails[0]) record_failure(P, b, GATO_STATUS_FACTORIZATION, 0, GATO_BLOCK_Q, fails[0], 0);
     else if (fails[1]) record_failure(P, b, GATO_STATUS_FACTORIZATION, P.N, GATO_BLOCK_Q, fails[1], 0);
@@ -749,6 +777,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_schur(SolveParams P)
   if (wg >= (int64_t)P.M * nb) return;
   const int b = (int)(wg / nb), k = (int)(wg % nb);
   if (!P.si[b * SI_WORDS + SI_ACTIVE]) return;
+  if (P.fused && P.si[b * SI_WORDS + SI_DIAG]) return;   // formed inside k_pcg_q (schur_quad.cuh)
   SchurSmem<NX, NU>& S = reinterpret_cast<SchurSmem<NX, NU>*>(schur_smem_raw)[warp];
   constexpr int HS = hinv_stride(NX, NU);
   constexpr int TRI = NX * (NX + 1) / 2;

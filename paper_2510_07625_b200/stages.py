@@ -85,7 +85,7 @@ def first_iteration_stages(problem: ProblemSpec, X, U, settings: SolverSettings 
     st = _as_settings(settings) if settings is not None else SolverSettings()
     N, n, m = problem.horizon, problem.model.state_dim, problem.model.control_dim
     one = dataclasses.replace(st, max_sqp_iterations=1, step_tolerance=None)
-    eng = BatchEngine(problem.model, 1, N, problem.timestep, one)
+    eng = BatchEngine(problem.model, 1, N, problem.timestep, one, stage_arrays=True)
     try:
         eng.solve(pack_problems([problem], [(np.asarray(X, dtype=float), np.asarray(U, dtype=float))], [st.rho_init]))
         g = {k: eng.scratch(k) for k in ("A", "B", "e", "grad", "hinv", "Sdiag", "Soff", "Linv", "gamma", "lam",

@@ -32,7 +32,7 @@ def stage_report(name):
     N, n, m = problem.horizon, problem.model.state_dim, problem.model.control_dim
     import dataclasses
     st1 = dataclasses.replace(st, max_sqp_iterations=1, step_tolerance=None)
-    eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, st1)
+    eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, st1, stage_arrays=True)
     packed = pack_problems([problem], [(g["X0"], g["U0"])], [st.rho_init])
     eng.solve(packed)
     got = {k: eng.scratch(k) for k in ("A", "B", "e", "grad", "hinv", "Sdiag", "Soff", "Linv", "gamma", "lam",

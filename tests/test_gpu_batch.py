@@ -151,7 +151,7 @@ def test_baseline_size_properties(M, N, h, kind):
     st = workloads.fixed_budget_settings(iters)
     eng = gb.BatchEngine(gb.Iiwa14(), M, N, h, st)
     try:
-        one = gb.BatchEngine(gb.Iiwa14(), M, N, h, dataclasses.replace(st, max_sqp_iterations=1))
+        one = gb.BatchEngine(gb.Iiwa14(), M, N, h, dataclasses.replace(st, max_sqp_iterations=1), stage_arrays=True)
         try:
             one.solve(batch)
             n, m = 14, 7

@@ -359,3 +359,49 @@ def test_diagonal_weight_shortcut_is_bitwise_the_dense_schur_products(tmp_path):
     assert np.all(a["status"] == 0)
     for key in ("X", "U", "pcg", "alpha"):
         assert np.array_equal(a[key], c[key]), key
+
+
+@pytest.mark.parametrize("kind,M,N,h,iters", [("reach", 3, 8, 0.02, 3), ("reach", 2, 33, 0.02, 2), ("track", 4, 32, 0.02, 2),
+                                               ("reach", 5, 64, 0.05, 3), ("reach", 2, 1, 0.02, 2), ("reach", 3, 9, 0.02, 2)])
+def test_fused_schur_pcg_is_bitwise_the_unfused_path(kind, M, N, h, iters):
+    """Solves with diagonal weights form their Schur system inside the PCG kernel (csrc/schur_quad.cuh): no
+    k_schur, no matrix record.  Every entry is computed with k_schur's operations in k_schur's order, so the
+    fused run must equal the run with the separate kernel (stage_arrays=True) bit for bit -- trajectories,
+    every trace field, PCG counts."""
+    batch = workloads.iiwa14_track_arrays(M, N, h) if kind == "track" else workloads.iiwa14_reach_arrays(M, N)
+    st = workloads.fixed_budget_settings(iters)
+    fused = gb.BatchEngine(gb.Iiwa14(), M, N, h, st)
+    plain = gb.BatchEngine(gb.Iiwa14(), M, N, h, st, stage_arrays=True)
+    try:
+        a, b = fused.solve(batch), plain.solve(batch)
+        assert fused.launch_count() == plain.launch_count()
+    finally:
+        fused.close()
+        plain.close()
+    assert np.all(a.info[:, _lib.INFO_STATUS] == 0)
+    assert np.array_equal(a.trace, b.trace, equal_nan=True), "trace (merits, PCG counts, step lengths)"
+    assert np.array_equal(a.X, b.X) and np.array_equal(a.U, b.U)
+    assert np.array_equal(a.info, b.info)
+
+
+def test_fused_and_unfused_solves_share_a_batch():
+    """A batch that mixes diagonal weights (fused path) with dense SPD weights (k_schur + record): each solve equals
+    its single-solve result bit for bit."""
+    M, N, h = 4, 16, 0.02
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    rng = np.random.default_rng(5)
+    G = rng.standard_normal((14, 14))
+    batch.Q[1] = batch.Q[1] + 0.05 * (G @ G.T)           # dense SPD
+    batch.R[3] = batch.R[3] + 1e-4 * np.ones((7, 7))      # dense SPD
+    st = workloads.fixed_budget_settings(3)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, h, st)
+    one = gb.BatchEngine(gb.Iiwa14(), 1, N, h, st)
+    try:
+        full = eng.solve(batch)
+        assert np.all(full.info[:, _lib.INFO_STATUS] == 0)
+        for b in range(M):
+            single = one.solve(batch.slice(b, b + 1))
+            assert np.array_equal(single.X[0], full.X[b]) and np.array_equal(single.trace[0], full.trace[b], equal_nan=True)
+    finally:
+        eng.close()
+        one.close()

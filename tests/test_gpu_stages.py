@@ -41,7 +41,7 @@ def test_first_iteration_stages_match_reference(name):
     problem, st = product_problem(g), product_settings(g)
     N, n, m = problem.horizon, problem.model.state_dim, problem.model.control_dim
     one = dataclasses.replace(st, max_sqp_iterations=1, step_tolerance=None)
-    eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, one)
+    eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, one, stage_arrays=True)
     try:
         eng.solve(pack_problems([problem], [(g["X0"], g["U0"])], [st.rho_init]))
         got = {k: eng.scratch(k) for k in ("A", "B", "e", "grad", "hinv", "Sdiag", "Soff", "Linv", "Lfac", "gamma", "gammaw",
@@ -88,7 +88,7 @@ def test_whitened_preconditioner_equals_explicit_stair_blocks(name):
     problem, st = product_problem(g), product_settings(g)
     N, n = problem.horizon, problem.model.state_dim
     one = dataclasses.replace(st, max_sqp_iterations=1, step_tolerance=None)
-    eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, one)
+    eng = gb.BatchEngine(problem.model, 1, N, problem.timestep, one, stage_arrays=True)
     try:
         eng.solve(pack_problems([problem], [(g["X0"], g["U0"])], [st.rho_init]))
         D = dinv_from_factor(eng.scratch("Linv"), N + 1, n)
