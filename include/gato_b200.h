@@ -88,6 +88,8 @@ extern "C" {
 /* gato_config.flags */
 #define GATO_FLAG_UNFUSED 1 /* keep form_schur in its own kernel and write the plain stage arrays (Sdiag, Soff, Linv,
                                Lfac, the matrix record) even where the PCG kernel could form the system itself */
+#define GATO_FLAG_FUSED 2   /* form the Schur system inside the PCG kernel wherever that kernel supports it, also for
+                               batches below the size from which it pays (default: decided by batch x horizon) */
 
 typedef struct gato_config {
   int32_t abi_version; /* GATO_ABI_VERSION */

@@ -39,6 +39,9 @@ bool select_ops(int model_id, const double* params, ModelOps* ops) {
   }
 }
 
+// batch x (horizon + 1) from which the fused Schur + PCG path is used (measured crossover, see gato_create)
+constexpr double kFusedMinBlockRows = 3000.0;
+
 struct Scratch {
   const char* name;
   void* ptr;
@@ -276,10 +279,18 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   P.regularize_r = cfg->regularize_r;
   P.retry_limit = cfg->pcg_retry_limit;
   P.dense_schur = env_int("GATO_SCHUR_DENSE", 0);
-  // Schur formation fused into the PCG kernel (schur_quad.cuh) wherever k_pcg_q runs; GATO_FUSED=0, the
-  // config flag GATO_FLAG_UNFUSED or GATO_SCHUR_DENSE=1 keep k_schur + the matrix record (stage arrays for tests)
-  P.fused = (env_int("GATO_FUSED", 1) && !(cfg->flags & GATO_FLAG_UNFUSED) && !P.dense_schur &&
-             h->ops.pcg_fused_ok((int)N)) ? 1 : 0;
+  // Schur formation fused into the PCG kernel (schur_quad.cuh) wherever k_pcg_q runs and it pays; GATO_FUSED=0,
+  // the config flag GATO_FLAG_UNFUSED or GATO_SCHUR_DENSE=1 keep k_schur + the matrix record (stage arrays for
+  // tests), GATO_FUSED=2 forces the fused path.  The rule (scripts/fused_crossover.py, profiles/r02_fused_crossover.csv):
+  // k_schur spreads M (N + 1) block rows over the whole GPU (one warp each), the fused phase handles a solve's
+  // block rows on the one SM that then runs its PCG -- so the fused path wins once the batch is large enough to
+  // keep the whole GPU busy with k_schur anyway, and loses in the latency regime (few solves).
+  {
+    const int mode = (cfg->flags & GATO_FLAG_FUSED) ? 2 : env_int("GATO_FUSED", 1);
+    const bool can = !(cfg->flags & GATO_FLAG_UNFUSED) && !P.dense_schur && h->ops.pcg_fused_ok((int)N);
+    const bool pays = (double)M * (double)(N + 1) >= kFusedMinBlockRows;
+    P.fused = (can && (mode == 2 || (mode == 1 && pays))) ? 1 : 0;
+  }
   P.h = cfg->timestep;
   P.pcg_tol = cfg->pcg_tolerance;
   P.mu = cfg->mu;

@@ -77,7 +77,7 @@ def _torch():
 
 
 def make_config(model, M: int, N: int, timestep: float, settings: SolverSettings,
-                loop_mode: int = 0, stage_arrays: bool = False) -> _lib.GatoConfig:
+                loop_mode: int = 0, stage_arrays: bool = False, fused: bool | None = None) -> _lib.GatoConfig:
     model_id, params = device_model(model)
     cfg = _lib.GatoConfig()
     cfg.abi_version = _lib.ABI_VERSION
@@ -93,7 +93,7 @@ def make_config(model, M: int, N: int, timestep: float, settings: SolverSettings
     cfg.regularize_r = int(settings.regularize_r)
     cfg.pcg_retry_limit = settings.pcg_retry_limit
     cfg.loop_mode = loop_mode
-    cfg.flags = _lib.FLAG_UNFUSED if stage_arrays else 0
+    cfg.flags = _lib.FLAG_UNFUSED if (stage_arrays or fused is False) else (_lib.FLAG_FUSED if fused else 0)
     cfg.timestep = float(timestep)
     cfg.pcg_tolerance = settings.pcg.tolerance
     cfg.mu = settings.line_search.mu
@@ -112,10 +112,12 @@ class BatchEngine:
     """gato_create + gato_bind for one configuration; solve() is H2D -> gato_solve -> D2H."""
 
     def __init__(self, model, M: int, N: int, timestep: float, settings: SolverSettings,
-                 device: int | None = None, loop_mode: int = 0, stage_arrays: bool = False):
+                 device: int | None = None, loop_mode: int = 0, stage_arrays: bool = False,
+                 fused: bool | None = None):
         """``stage_arrays=True`` keeps the Schur formation in its own kernel so that ``scratch()`` can read
         Sdiag, Soff, Linv, Lfac and the matrix record (stage-by-stage parity tests); by default solves with
-        diagonal weights form their Schur system inside the PCG kernel and those arrays are not written."""
+        diagonal weights form their Schur system inside the PCG kernel (from batch x horizon ~ 3000 block rows
+        on, where it pays; ``fused=True`` / ``False`` forces either path) and those arrays are not written."""
         torch = _torch()
         self.lib = _lib.load()
         self.torch = torch
@@ -156,7 +158,7 @@ class BatchEngine:
             self.pin = {name: view(self.pinned, name) for name in self.layout}
             self.pin_np = {name: t.numpy() for name, t in self.pin.items()}
             self.stream = torch.cuda.Stream(device=self.device)
-            cfg = make_config(model, M, N, timestep, settings, loop_mode, stage_arrays)
+            cfg = make_config(model, M, N, timestep, settings, loop_mode, stage_arrays, fused)
             handle = C.c_void_p()
             rc = self.lib.gato_create(C.byref(cfg), C.byref(handle))
             self.handle = handle

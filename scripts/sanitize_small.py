@@ -19,9 +19,11 @@ from conftest import load_golden, product_problem, product_settings  # noqa: E40
 # iiwa14: quadrant PCG (N=8, N=40, N=64 = the full CTA; with GATO_PCG_Q=1 in the environment N=8 runs the
 # row-resident k_pcg_rt instead), fat-thread PCG with O^ and L resident (N=70), O^ resident only (N=100),
 # everything in global memory (N=150); the control-step call, best-of-batch, hypothesis selection
-for N, iters in ((8, 2), (40, 1), (64, 1), (70, 1), (100, 1), (150, 1)):
+# ... and the Schur phase fused into k_pcg_q (fused=True; N = 9: a warp with idle quads, N = 64: the full CTA)
+for N, iters, fused in ((8, 2, None), (40, 1, None), (64, 1, None), (70, 1, None), (100, 1, None), (150, 1, None),
+                        (9, 2, True), (33, 1, True), (64, 1, True)):
     batch = workloads.iiwa14_reach_arrays(3, N)
-    eng = gb.BatchEngine(gb.Iiwa14(), 3, N, 0.02, workloads.fixed_budget_settings(iters), loop_mode=3)
+    eng = gb.BatchEngine(gb.Iiwa14(), 3, N, 0.02, workloads.fixed_budget_settings(iters), loop_mode=3, fused=fused)
     res = eng.solve(batch)
     eng.shift_warm_start()
     eng.stream.synchronize()

@@ -370,7 +370,7 @@ def test_fused_schur_pcg_is_bitwise_the_unfused_path(kind, M, N, h, iters):
     every trace field, PCG counts."""
     batch = workloads.iiwa14_track_arrays(M, N, h) if kind == "track" else workloads.iiwa14_reach_arrays(M, N)
     st = workloads.fixed_budget_settings(iters)
-    fused = gb.BatchEngine(gb.Iiwa14(), M, N, h, st)
+    fused = gb.BatchEngine(gb.Iiwa14(), M, N, h, st, fused=True)
     plain = gb.BatchEngine(gb.Iiwa14(), M, N, h, st, stage_arrays=True)
     try:
         a, b = fused.solve(batch), plain.solve(batch)
@@ -394,8 +394,8 @@ def test_fused_and_unfused_solves_share_a_batch():
     batch.Q[1] = batch.Q[1] + 0.05 * (G @ G.T)           # dense SPD
     batch.R[3] = batch.R[3] + 1e-4 * np.ones((7, 7))      # dense SPD
     st = workloads.fixed_budget_settings(3)
-    eng = gb.BatchEngine(gb.Iiwa14(), M, N, h, st)
-    one = gb.BatchEngine(gb.Iiwa14(), 1, N, h, st)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, h, st, fused=True)
+    one = gb.BatchEngine(gb.Iiwa14(), 1, N, h, st, fused=True)
     try:
         full = eng.solve(batch)
         assert np.all(full.info[:, _lib.INFO_STATUS] == 0)
