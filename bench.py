@@ -506,9 +506,18 @@ class GpuArm:
         }
         fam_ms = {"linearize": kern_ms["linearize"], "schur": kern_ms["schur"] + kern_ms["hessinv"],
                   "pcg": kern_ms["pcg"], "linesearch": kern_ms["linesearch"]}
+        fused = self.eng.fused
+        if fused:
+            # the Schur system is formed inside the PCG kernel: its flops and the (empty) k_schur launch belong to
+            # that kernel's family; k_hessinv stays on its own
+            fam_flops["pcg"] += M * K * (N * F_SCHUR + (N + 1) * F_PREC)
+            fam_flops["schur"] = M * K * F_HESS
+            fam_ms["pcg"] += kern_ms["schur"]
+            fam_ms["schur"] = kern_ms["hessinv"]
         dominant = max(fam_ms, key=fam_ms.get)
-        pcg_kernel = "k_pcg_q" if N <= 64 else "k_pcg"
-        names = {"linearize": "k_lin_tangent_iiwa", "schur": "k_schur", "pcg": pcg_kernel, "linesearch": "k_linesearch"}
+        pcg_kernel = ("k_pcg_q<fused Schur>" if fused else "k_pcg_q") if N <= 64 else "k_pcg"
+        names = {"linearize": "k_lin_tangent_iiwa", "schur": "k_hessinv" if fused else "k_schur", "pcg": pcg_kernel,
+                 "linesearch": "k_linesearch"}
         achieved = fam_flops[dominant] / (fam_ms[dominant] * 1e-3) / 1e12
         total_flops = float(np.sum([flops_solve_iteration(N, p) for p in P_prof.reshape(-1)]))
         # compulsory HBM bytes of a solve-iteration in the fused-in-L2 design
@@ -525,6 +534,7 @@ class GpuArm:
                     "algorithmic_bytes_per_step": alg_bytes},
             "step": {"achieved": total_flops / total_s / 1e12, "unit": "TFLOP/s",
                      "frac": total_flops / total_s / 1e12 / fp64_peak, "algorithmic_flops_per_step": total_flops},
+            "fused_schur_pcg": bool(fused),
             "kernel_ms_per_step": {k: round(v, 5) for k, v in kern_ms.items()},
             "kernel_tflops": {k: fam_flops[k] / (fam_ms[k] * 1e-3) / 1e12 for k in fam_flops},
         }
@@ -683,6 +693,7 @@ def run_gpu_arm(args, rank, local_rank, world):
             line[k] = rec[k]
         line["clocks"] = clocks.summary()
         line["roofline"] = {k: v for k, v in rec["roofline"].items() if k not in ("kernel_ms_per_step", "kernel_tflops")}
+        line["fused_schur_pcg"] = rec["roofline"]["fused_schur_pcg"]
         line["kernel_ms_per_step"] = rec["roofline"]["kernel_ms_per_step"]
         line["kernel_tflops"] = rec["roofline"]["kernel_tflops"]
         line["pcg_iterations_mean"] = rec["pcg_iterations_mean"]

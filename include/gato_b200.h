@@ -175,6 +175,9 @@ int gato_best_of_batch(gato_handle* h, void* stream, int32_t* best_index, double
 int gato_pending(gato_handle* h, void* stream, int32_t* pending);
 int gato_resume(gato_handle* h, void* stream, int32_t passes);
 int gato_loop_mode(const gato_handle* h);
+/* 1 if this handle forms the Schur system of solves with diagonal weights inside its PCG kernel (no k_schur, no
+ * matrix record for them; GATO_FLAG_* and the batch size decide), 0 if every solve goes through k_schur. */
+int gato_fused(const gato_handle* h);
 /* Device pointer + element count of an internal stage array, for stage-by-stage parity
  * tests: "A","B","e","grad","hinv","Sdiag","Soff","Dinv","gamma","lam","dX","dU","merits",
  * "viols","state","pcg_iters". Valid until gato_destroy. */

@@ -56,6 +56,7 @@ EXPORTS = {
     "gato_pending": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
     "gato_resume": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "gato_loop_mode": (C.c_int, [C.c_void_p]),
+    "gato_fused": (C.c_int, [C.c_void_p]),
     "gato_scratch": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "gato_read_scratch": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64]),
     "gato_launch_count": (C.c_int64, [C.c_void_p]),

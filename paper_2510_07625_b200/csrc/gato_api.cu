@@ -569,11 +569,14 @@ int64_t gato_launch_count(const gato_handle* h) {
   unsigned int c[4] = {0, 0, 0, 0};
   if (cudaMemcpy(c, h->P.counters, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   // k_init + per pass: k_hessinv, linearisation (two kernels for iiwa14), k_schur, PCG, k_linesearch, k_update
-  const int per_pass = 5 + (h->ops.lin_scratch_bytes(1) > 0 ? 2 : 1);
+  // (with the fused Schur + PCG path the PCG step is two launches: the fused and the record-reading build)
+  const int per_pass = 5 + (h->ops.lin_scratch_bytes(1) > 0 ? 2 : 1) + (h->P.fused ? 1 : 0);
   return 1 + per_pass * (int64_t)c[3];
 }
 
 int gato_loop_mode(const gato_handle* h) { return h ? h->loop_mode : 0; }
+
+int gato_fused(const gato_handle* h) { return h ? h->P.fused : 0; }
 
 /* Same work as gato_solve in plain stream-launch mode, with CUDA events between the six kernels of
  * every pass: ms[0..5] = total device time of hessinv, linearize, schur, pcg, linesearch, update

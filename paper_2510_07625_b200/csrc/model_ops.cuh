@@ -154,7 +154,9 @@ cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
     const int qmode = pcg_use_q<Mdl>(P.N);
     const bool rt = pcg_use_rt<Mdl>(P.N);
     if (qmode == 2 || (qmode == 1 && !rt)) {
-      k_pcg_q<NX, NU><<<P.M, pcg_q_threads(P.N), pcg_q_smem_bytes<NX>(P.N), s>>>(P);
+      // with P.fused both builds run: every solve is taken by exactly one of them (SI_DIAG), the other exits at once
+      if (P.fused) k_pcg_q<NX, NU, true><<<P.M, pcg_q_threads(P.N), pcg_q_smem_bytes<NX>(P.N), s>>>(P);
+      k_pcg_q<NX, NU, false><<<P.M, pcg_q_threads(P.N), pcg_q_smem_bytes<NX>(P.N), s>>>(P);
       return cudaGetLastError();
     }
     if (rt) {
@@ -238,7 +240,10 @@ cudaError_t prepare_attrs(const SolveParams& P) {
   }
   if constexpr (NX >= 14) {
     if (pcg_use_q<Mdl>(P.N)) {
-      err = cudaFuncSetAttribute(k_pcg_q<NX, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      err = cudaFuncSetAttribute(k_pcg_q<NX, NU, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pcg_q_smem_bytes<NX>(P.N));
+      if (err != cudaSuccess) return err;
+      err = cudaFuncSetAttribute(k_pcg_q<NX, NU, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pcg_q_smem_bytes<NX>(P.N));
       if (err != cudaSuccess) return err;
     }

@@ -876,7 +876,10 @@ __host__ __device__ constexpr size_t pcg_q_smem_bytes(int N) {
   return 16 * 16 + xch + lbw + (mats > vecs ? mats : vecs);
 }
 
-template <int NX, int NU>
+// FUSED = true: the solves flagged SI_DIAG form their Schur system here (schur_quad.cuh); FUSED = false: the
+// solves whose system k_schur formed (all of them when P.fused = 0, the ones with general weights otherwise)
+// read the matrix record.  With P.fused both builds are launched and each solve is taken by exactly one.
+template <int NX, int NU, bool FUSED>
 __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
   static_assert(NX % 2 == 0, "state = [positions, velocities]");
   using L = PcgLayout<NX>;
@@ -903,7 +906,8 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
   double* R2 = mats + wreg;                             // packed L_k^-1: slot k = block row k + 1, slot N = block row 0
   // Fused mode (schur_quad.cuh): this CTA forms the Schur system of its solve itself -- no matrix record, no
   // k_schur.  CTA-uniform: the flag is written by k_hessinv, two kernels upstream.
-  const bool fused = P.fused && si[SI_DIAG];
+  constexpr bool fused = FUSED;
+  if ((P.fused && si[SI_DIAG] != 0) != FUSED) return;   // the other build's solve (CTA-uniform: written by k_hessinv)
   const double* LfS = mats;   // packed L_k for the exact-norm iterations: bulk-copied over the W region once it is free
   __shared__ __align__(8) unsigned long long fill_bar, lf_bar_mem;
   __shared__ QuadDiag<NX, NU> s_diag;
@@ -916,12 +920,12 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     s_fail = INT_MAX;
   }
   if (t < 16) red[t] = make_double2(0.0, 0.0);
-  if (fused) {
+  if constexpr (FUSED) {
     quad_schur_stage<NX, NU>(P, b, t, N, Wm, R2);   // A_k, B_k on their way into shared memory
     quad_diag_load<NX, NU>(P, b, t, s_diag);
   }
   __syncthreads();
-  if (!fused) {
+  if constexpr (!fused) {
     if (t == 0) {
       const unsigned bytes_off = (unsigned)((size_t)N * L::BSP * 8), bytes_tri = (unsigned)((size_t)nb * L::TRP * 8);
       mbar_expect(bar, bytes_off + bytes_tri);
@@ -1015,7 +1019,7 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     constexpr int JA = (NX * 4 + 6) / 7, JB = (NX * 11 + 13) / 14;   // n = 14: columns 0-7 | 8-10 | 11-13
     constexpr int TRI = NX * (NX + 1) / 2, EA = JA * (JA + 1) / 2, EB = JB * (JB + 1) / 2;
     double LC[TRI - EB], LB[EB - EA], LA[EA];
-    if (!fused) mbar_wait0(bar);
+    if constexpr (!fused) mbar_wait0(bar);
     load_cols(IntC<JB>{}, IntC<NX>{}, LC);
     load_cols(IntC<JA>{}, IntC<JB>{}, LB);
     whiten_cols(IntC<JB>{}, IntC<NX>{}, LC);
@@ -1294,7 +1298,7 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
     const int kr = e_kr[rd], i0 = e_i0[rd], i1 = i0 + HN;
     const bool knot = e_ok[rd] && kr < N;
     // phi_k = -A_k Q^-1: k_schur's array, or (fused mode, Q^-1 diagonal) the same products formed here
-    const bool fz = P.fused && si[SI_DIAG];   // = fused, re-read so that it is not live across the iteration
+    constexpr bool fz = FUSED;
     const double* Ph = (fz ? P.A : P.Soff) + ((size_t)b * N + (knot ? kr : 0)) * BS;
     const double sc0 = fz ? -s_diag.qd[i0] : 1.0, sc1 = fz ? -s_diag.qd[i1] : 1.0;
     const double* Ri = hinv + 2 * BS;

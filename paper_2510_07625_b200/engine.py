@@ -194,6 +194,11 @@ class BatchEngine:
     def loop_mode(self) -> int:
         return int(self.lib.gato_loop_mode(self.handle))
 
+    @property
+    def fused(self) -> bool:
+        """True if solves with diagonal weights form their Schur system inside the PCG kernel (gato_fused)."""
+        return bool(self.lib.gato_fused(self.handle))
+
     # -- staged steps (all asynchronous on self.stream) ---------------------------- #
     def _span(self, first: str, last: str) -> slice:
         return slice(self.offsets[first][0], self.offsets[last][0] + self.offsets[last][1])

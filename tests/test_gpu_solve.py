@@ -374,7 +374,8 @@ def test_fused_schur_pcg_is_bitwise_the_unfused_path(kind, M, N, h, iters):
     plain = gb.BatchEngine(gb.Iiwa14(), M, N, h, st, stage_arrays=True)
     try:
         a, b = fused.solve(batch), plain.solve(batch)
-        assert fused.launch_count() == plain.launch_count()
+        assert fused.fused and not plain.fused
+        assert fused.launch_count() == plain.launch_count() + iters   # one more launch per pass: the two PCG builds
     finally:
         fused.close()
         plain.close()
