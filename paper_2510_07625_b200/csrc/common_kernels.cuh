@@ -15,6 +15,7 @@ __global__ void k_init(SolveParams P) {
     P.counters[1] = 0;
     P.counters[2] = (unsigned)P.M;
     P.counters[3] = 0;
+    P.counters[4] = 0;
   }
   if (b >= P.M) return;
   P.sd[b * SD_WORDS + SD_RHO] = P.rho_init[b];

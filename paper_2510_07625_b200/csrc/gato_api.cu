@@ -326,6 +326,7 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   ALLOC(sd, M * SD_WORDS);
   ALLOC(si, M * SI_WORDS);
   ALLOC(pcg_iters, M * P.max_it);
+  ALLOC(schur_list, M);
   ALLOC(counters, 8);
 #undef ALLOC
   if (rc != GATO_OK) return rc;

@@ -75,7 +75,13 @@ cudaError_t launch_schur(const SolveParams& P, cudaStream_t s) {
   constexpr int WARPS = kSchurWarps;
   const size_t smem = WARPS * sizeof(SchurSmem<Mdl::NX, Mdl::NU>);
   const int64_t warps = (int64_t)P.M * (P.N + 1);
-  k_schur<Mdl::NX, Mdl::NU, WARPS><<<(unsigned)((warps + WARPS - 1) / WARPS), WARPS * 32, smem, s>>>(P);
+  int64_t grid = (warps + WARPS - 1) / WARPS;
+  if (P.fused) {   // only the solves with general weights, listed by k_hessinv
+    if (grid > 8 * 148) grid = 8 * 148;
+    k_schur_listed<Mdl::NX, Mdl::NU, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(P);
+  } else {
+    k_schur<Mdl::NX, Mdl::NU, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(P);
+  }
   return cudaGetLastError();
 }
 
@@ -226,6 +232,9 @@ cudaError_t prepare_attrs(const SolveParams& P) {
     if (err != cudaSuccess) return err;
   }
   err = cudaFuncSetAttribute(k_schur<NX, NU, kSchurWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kSchurWarps * sizeof(SchurSmem<NX, NU>)));
+  if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(k_schur_listed<NX, NU, kSchurWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kSchurWarps * sizeof(SchurSmem<NX, NU>)));
   if (err != cudaSuccess) return err;
   {

@@ -42,8 +42,8 @@ struct SolveParams {
   int32_t* info;
   // scratch
   double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Linv, *Lfac, *pmats, *gamma, *gammaw, *lbw, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
-  int32_t *si, *pcg_iters;
-  unsigned int* counters;  // [0] active count, [1] ticket, [2] pending solves, [3] passes run
+  int32_t *si, *pcg_iters, *schur_list;   // schur_list: solves of this pass that need k_schur (P.fused only)
+  unsigned int* counters;  // [0] active count, [1] ticket, [2] pending solves, [3] passes run, [4] entries of schur_list
 };
 
 // doubles per solve in hinv: [Qs^-1 | Qt^-1 | Rs^-1], padded to an even count (16-byte rows)
@@ -266,7 +266,10 @@ __global__ void __launch_bounds__(96) k_hessinv(SolveParams P) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    P.si[b * SI_WORDS + SI_DIAG] = !(offdiag[0] | offdiag[1] | offdiag[2] | fails[0] | fails[1] | fails[2]);
+    const int diag = !(offdiag[0] | offdiag[1] | offdiag[2] | fails[0] | fails[1] | fails[2]);
+    P.si[b * SI_WORDS + SI_DIAG] = diag;
+    if (P.fused && !diag && !(fails[0] | fails[1] | fails[2]))   // k_schur's solve (order of the list: irrelevant)
+      P.schur_list[atomicAdd(&P.counters[4], 1u)] = b;
     // reporting order of form_schur: Q_0 .. Q_N first, then R_0 (qpform.py:305-311)
     if (fails[0]) record_failure(P, b, GATO_STATUS_FACTORIZATION, 0, GATO_BLOCK_Q, fails[0], 0);
     else if (fails[1]) record_failure(P, b, GATO_STATUS_FACTORIZATION, P.N, GATO_BLOCK_Q, fails[1], 0);
@@ -766,19 +769,12 @@ struct SchurSmem {
   double qk[NX], qj[NX], rj[NU + (NU & 1)], dxk[NX], dxj[NX], gk[NX];
 };
 
-template <int NX, int NU, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_schur(SolveParams P) {
-  extern __shared__ __align__(16) double schur_smem_raw[];
+// one block row (b, k) by one warp; S: the warp's shared-memory scratch
+template <int NX, int NU>
+__device__ __forceinline__ void schur_block_row(const SolveParams& P, SchurSmem<NX, NU>& S, int b, int k, int lane) {
   using L = PcgLayout<NX>;
   constexpr int HALF = NX / 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t wg = (int64_t)blockIdx.x * WARPS + warp;
   const int nb = P.N + 1;
-  if (wg >= (int64_t)P.M * nb) return;
-  const int b = (int)(wg / nb), k = (int)(wg % nb);
-  if (!P.si[b * SI_WORDS + SI_ACTIVE]) return;
-  if (P.fused && P.si[b * SI_WORDS + SI_DIAG]) return;   // formed inside k_pcg_q (schur_quad.cuh)
-  SchurSmem<NX, NU>& S = reinterpret_cast<SchurSmem<NX, NU>*>(schur_smem_raw)[warp];
   constexpr int HS = hinv_stride(NX, NU);
   constexpr int TRI = NX * (NX + 1) / 2;
   const double* Qi = P.hinv + (size_t)b * HS;
@@ -1054,6 +1050,35 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_schur(SolveParams P)
   }
 }
 
+// every block row of every active solve: one warp each
+template <int NX, int NU, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_schur(SolveParams P) {
+  extern __shared__ __align__(16) double schur_smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wg = (int64_t)blockIdx.x * WARPS + warp;
+  const int nb = P.N + 1;
+  if (wg >= (int64_t)P.M * nb) return;
+  const int b = (int)(wg / nb), k = (int)(wg % nb);
+  if (!P.si[b * SI_WORDS + SI_ACTIVE]) return;
+  schur_block_row<NX, NU>(P, reinterpret_cast<SchurSmem<NX, NU>*>(schur_smem_raw)[warp], b, k, lane);
+}
+
+// P.fused: only the solves k_hessinv has listed (active, general weights: counters[4] entries of schur_list) are
+// this kernel's -- usually none.  A small fixed grid strides over their block rows, so that the common case
+// costs one load per warp instead of a CTA per block row of the whole batch.
+template <int NX, int NU, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_schur_listed(SolveParams P) {
+  extern __shared__ __align__(16) double schur_smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = P.N + 1;
+  const int64_t total = (int64_t)P.counters[4] * nb;
+  for (int64_t wg = (int64_t)blockIdx.x * WARPS + warp; wg < total; wg += (int64_t)gridDim.x * WARPS) {
+    const int b = P.schur_list[wg / nb], k = (int)(wg % nb);
+    schur_block_row<NX, NU>(P, reinterpret_cast<SchurSmem<NX, NU>*>(schur_smem_raw)[warp], b, k, lane);
+    __syncwarp();
+  }
+}
+
 template <int NX>
 __device__ __forceinline__ double dot_row(const double* __restrict__ row, const double* __restrict__ v) {
   double acc = 0.0;
@@ -1204,6 +1229,7 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
       __threadfence();
       const unsigned n_active = atomicExch(&P.counters[0], 0u);
       P.counters[1] = 0;
+      P.counters[4] = 0;         // schur_list is rebuilt by the next pass's k_hessinv
       P.counters[2] = n_active;  // host-visible "pending" word
       P.counters[3] += 1;        // passes executed
       if (use_cond) cudaGraphSetConditional(cond, n_active > 0 ? 1u : 0u);
