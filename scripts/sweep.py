@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--repeats", type=int, default=5)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--cpu", action="store_true",
-                    help="add the CPU reference port (oracle, forked pool over all host cores): one wave of "
+                    help="add the CPU reference (baseline/_ref, else its oracle port; forked pool over all host cores): one wave of "
                          "min(M, cores) solves is timed per horizon and scaled by ceil(M / cores) waves "
                          "(SURVEY.md 8d: prefix + linear scaling for cells that would take minutes)")
     args = ap.parse_args()
@@ -63,9 +63,9 @@ def main():
                 count = min(M, cores)
                 if (N, count) not in cpu_wave:
                     w = dict(M=count, N=N, h=h, kind="reach", sqp=args.iters)
-                    wave_batch = workloads.iiwa14_reach_arrays(count, N)
-                    bench.cpu_step(w, wave_batch, count, cores)              # warm-up (imports, pool)
-                    cpu_wave[(N, count)] = 1e3 * bench.cpu_step(w, wave_batch, count, cores)
+                    arm = bench.CpuArm("sweep", w)       # the unmodified reference (baseline/_ref) if installed
+                    arm.step()                                               # warm-up (imports, pool)
+                    cpu_wave[(N, count)] = 1e3 * arm.step()[0]
                 cpu_ms = cpu_wave[(N, count)] * math.ceil(M / cores)
                 row += f",{cpu_ms:.1f},{cores},{cpu_ms / med:.0f}"
             rows.append(row)
