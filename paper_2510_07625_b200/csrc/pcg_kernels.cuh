@@ -26,6 +26,7 @@
 //   k_pcg     (any n, N + 1 <= 256)  one thread per block row, O^ and L in shared memory (or global
 //             memory when the horizon does not fit), 16-byte row loads, O^_k^T applied by rows.
 #pragma once
+#include <cstdio>
 #include "solver_kernels.cuh"
 #include "schur_quad.cuh"
 
@@ -92,6 +93,9 @@ __device__ __forceinline__ void pcg_finish(const SolveParams& P, int b, int32_t*
 struct Reducer8 {
   double2* red;  // [2][8], zero-initialised (slots of absent warps stay zero)
   int flip;
+#ifdef GATO_PCG_TIMING
+  long long t_tree = 0, t_bar = 0, t_tail = 0;   // shuffle tree | store + barrier wait | loads + cross-warp tree
+#endif
   __device__ __forceinline__ double2 finish(double2* buf) {
     __syncthreads();
     const double2 v0 = buf[0], v1 = buf[1], v2 = buf[2], v3 = buf[3], v4 = buf[4], v5 = buf[5], v6 = buf[6],
@@ -100,12 +104,29 @@ struct Reducer8 {
                         ((v0.y + v1.y) + (v2.y + v3.y)) + ((v4.y + v5.y) + (v6.y + v7.y)));
   }
   __device__ __forceinline__ double sum1(double a) {
+#ifdef GATO_PCG_TIMING
+    const long long c0 = clock64();
+#endif
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     double2* buf = red + flip * 8;
     flip ^= 1;
+#ifdef GATO_PCG_TIMING
+    const long long c1 = clock64();
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5].x = a;
+    __syncthreads();
+    const long long c2 = clock64();
+    const double2 v0 = buf[0], v1 = buf[1], v2 = buf[2], v3 = buf[3], v4 = buf[4], v5 = buf[5], v6 = buf[6], v7 = buf[7];
+    const double out = ((v0.x + v1.x) + (v2.x + v3.x)) + ((v4.x + v5.x) + (v6.x + v7.x));
+    const long long c3 = clock64() + (out == 1.2345e300);
+    t_tree += c1 - c0;
+    t_bar += c2 - c1;
+    t_tail += c3 - c2;
+    return out;
+#else
     if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5].x = a;
     return finish(buf).x;
+#endif
   }
   // lanes 0-15 reduce a, lanes 16-31 reduce b after one crossed exchange: 5 shuffles for 2 values
   __device__ __forceinline__ double2 sum2(double a, double b) {
@@ -1165,10 +1186,21 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
 #pragma unroll
     for (int i = 0; i < HN; ++i) p[i] = r[i] - tot[i];   // z^ = (I - O^) r^
     const int cap = P.pcg_cap;
+#ifdef GATO_PCG_TIMING
+    long long tacc[7] = {0, 0, 0, 0, 0, 0, 0};
+#define TCK(i) { const long long tn = clock64(); tacc[i] += tn - tlast; tlast = tn; }
+#else
+#define TCK(i)
+#endif
     for (int it = 1; it <= cap; ++it) {
+#ifdef GATO_PCG_TIMING
+      long long tlast = clock64();
+#endif
       publish(p);
       __syncthreads();
+      TCK(0)
       products(w);
+      TCK(1)
       const double curv = R.sum1(hold ? dot(p, p) + (isw ? 2.0 * dot(p, w) : 0.0) : 0.0);   // p^ . (I + O^) p^
       if (curv <= 0.0) {  // blocktri.py:158-161
         breakdown = it;
@@ -1179,6 +1211,7 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
         its = cap;
         break;
       }
+      TCK(2)
       total(w, tot);
       const double a = rz / curv;
 #pragma unroll
@@ -1188,11 +1221,14 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
       }
       publish(r);
       __syncthreads();
+      TCK(3)
       products(w);
+      TCK(4)
       const double rr_own = hold ? dot(r, r) : 0.0;
       double n2 = lbw * rr_own;   // lower bound of this half row's share of ||L_k r^_k||^2
       if (exact) n2 = tri_rows_norm2(xv);
       double2 rr = R.sum2(rr_own - ((hold && isw) ? 2.0 * dot(r, w) : 0.0), n2);
+      TCK(5)
       total(w, tot);
       its = it;
       if (!exact && rr.y <= tol2) {   // the bound no longer excludes convergence: exact norm from now on
@@ -1224,7 +1260,16 @@ __global__ void __launch_bounds__(kPcgQMaxThreads, 1) k_pcg_q(SolveParams P) {
       for (int i = 0; i < HN; ++i) p[i] = (r[i] - tot[i]) + beta * p[i];   // z^ + beta p^
       rz = rr.x;
       inv_rz = 1.0 / rz;
+      TCK(6)
     }
+#ifdef GATO_PCG_TIMING
+    if (t == 0 && b == 0)
+      printf("pcg timing N=%d its=%d  cycles/iteration: publish+bar %lld | products %lld | dot+sum1 %lld | total+div+update+publish+bar %lld | products %lld | dot+sum2 %lld | total+beta+p %lld\n",
+             N, its, tacc[0] / its, tacc[1] / its, tacc[2] / its, tacc[3] / its, tacc[4] / its, tacc[5] / its, tacc[6] / its);
+    if (t == 0 && b == 0)
+      printf("   sum1 calls (all): shuffle tree %lld | store + barrier %lld | loads + cross-warp tree %lld  cycles per PCG iteration\n",
+             R.t_tree / its, R.t_bar / its, R.t_tail / its);
+#endif
   }
 
   if (lf_pending) mbar_wait0(lf_bar);   // no bulk copy may be in flight when its target is reused or the CTA exits
