@@ -43,7 +43,7 @@ struct SolveParams {
   // scratch
   double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Linv, *Lfac, *pmats, *gamma, *gammaw, *lbw, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
   int32_t *si, *pcg_iters, *schur_list;   // schur_list: solves of this pass that need k_schur (P.fused only)
-  unsigned int* counters;  // [0] active count, [1] ticket, [2] pending solves, [3] passes run, [4] entries of schur_list
+  unsigned int* counters;  // [0] arrivals + [1] active count (one 64-bit word), [2] pending solves, [3] passes run, [4] entries of schur_list
 };
 
 // doubles per solve in hinv: [Qs^-1 | Qt^-1 | Rs^-1], padded to an even count (16-byte rows)
@@ -1144,9 +1144,16 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
                                              cudaGraphConditionalHandle cond, int use_cond, unsigned n_solves) {
   int32_t* si = P.si + b * SI_WORDS;
   __shared__ double s_alpha;
-  __shared__ int s_accept;
-  const int active = si[SI_ACTIVE];
-  const int skip = si[SI_SKIP_LS];
+  __shared__ int s_accept, s_state[2];
+  // the solve's state words as they were when the kernel started, the same for every thread: thread 0 rewrites
+  // them further down while other warps may not have looked yet
+  if (threadIdx.x == 0) {
+    s_state[0] = si[SI_ACTIVE];
+    s_state[1] = si[SI_SKIP_LS];
+  }
+  __syncthreads();
+  const int active = s_state[0];
+  const int skip = s_state[1];
   if (skip == 2) {   // tolerance exit at the very first iteration: patch merit(X0, U0) into its record
     if (threadIdx.x == 0) {
       const double m0 = __ldcg(&P.merits[(size_t)b * (P.C + 1) + P.C]);
@@ -1207,6 +1214,24 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
       si[SI_IT] = it + 1;
       if (it + 1 >= P.max_it) si[SI_ACTIVE] = 0;
     }
+  }
+  // One ticket per solve: a single 64-bit atomic carries the arrival count (low word, counters[0]) and the number
+  // of still-active solves (high word, counters[1]); the last arrival publishes the pass.  Thread 0 takes it as
+  // soon as its own state words are final, while the other threads apply the step.
+  if (threadIdx.x == 0) {
+    const unsigned long long still = si[SI_ACTIVE] ? 1ull : 0ull;
+    const unsigned long long old =
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.counters), (still << 32) + 1ull);
+    if ((unsigned)(old & 0xffffffffull) == n_solves - 1) {
+      const unsigned n_active = (unsigned)(old >> 32) + (unsigned)still;
+      *reinterpret_cast<volatile unsigned long long*>(P.counters) = 0ull;
+      P.counters[4] = 0;         // schur_list is rebuilt by the next pass's k_hessinv
+      P.counters[2] = n_active;  // host-visible "pending" word
+      P.counters[3] += 1;        // passes executed
+      if (use_cond) cudaGraphSetConditional(cond, n_active > 0 ? 1u : 0u);
+    }
+  }
+  if (active && !skip) {
     __syncthreads();
     if (s_accept) {
       const double alpha = s_alpha;
@@ -1217,22 +1242,6 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
       double* U = P.U + (size_t)b * nU;
       const double* dU = P.dU + (size_t)b * nU;
       for (int i = threadIdx.x; i < nU; i += blockDim.x) U[i] = __dadd_rn(U[i], __dmul_rn(alpha, dU[i]));
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int still = si[SI_ACTIVE];
-    if (still) atomicAdd(&P.counters[0], 1u);
-    __threadfence();
-    const unsigned ticket = atomicAdd(&P.counters[1], 1u);
-    if (ticket == n_solves - 1) {
-      __threadfence();
-      const unsigned n_active = atomicExch(&P.counters[0], 0u);
-      P.counters[1] = 0;
-      P.counters[4] = 0;         // schur_list is rebuilt by the next pass's k_hessinv
-      P.counters[2] = n_active;  // host-visible "pending" word
-      P.counters[3] += 1;        // passes executed
-      if (use_cond) cudaGraphSetConditional(cond, n_active > 0 ? 1u : 0u);
     }
   }
 }
