@@ -264,8 +264,8 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
     set_error(h, "batch, horizon, max_sqp_iterations must be >= 1 and timestep > 0");
     return GATO_E_INVALID;
   }
-  if (cfg->horizon + 1 > 256) {
-    set_error(h, "horizon too long: the PCG kernel runs one thread per block row, N + 1 <= 256");
+  if (cfg->horizon + 1 > 1024) {
+    set_error(h, "horizon too long: the PCG kernels run one thread per block row, N + 1 <= 1024");
     return GATO_E_INVALID;
   }
   SolveParams& P = h->P;
@@ -348,7 +348,15 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-  CK(h->ops.prepare(P));
+  {
+    cudaError_t perr = h->ops.prepare(P);
+    if (perr != cudaSuccess) {   // e.g. N + 1 > 256 with a state dimension whose exchange vectors exceed shared memory
+      set_error(h, std::string("kernel set-up failed (horizon too long for this model's shared-memory footprint?): ") +
+                       cudaGetErrorString(perr));
+      cudaGetLastError();
+      return GATO_E_INVALID;
+    }
+  }
   h->loop_mode = cfg->loop_mode ? cfg->loop_mode : env_int("GATO_LOOP_MODE", 1);
   return GATO_OK;
 }

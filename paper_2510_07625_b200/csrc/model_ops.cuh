@@ -127,6 +127,13 @@ PcgShape pcg_shape(int N, int M) {
   }
   PcgShape sh;
   sh.threads = pcg_threads(N);
+  if (sh.threads > 256) {   // long horizons: the 1024-thread build, matrices in global memory
+    sh.smem = false;
+    sh.lres = false;
+    sh.minb = 1;
+    sh.bytes = pcg_smem_bytes<NX>(N, false, false, 32);
+    return sh;
+  }
   const size_t with_mats = pcg_smem_bytes<NX>(N, true);
   sh.smem = with_mats <= kMaxSmem && env_int("GATO_PCG_GLOBAL", 0) == 0;
   sh.lres = false;
@@ -146,7 +153,8 @@ PcgShape pcg_shape(int N, int M) {
 template <class Mdl, class F>
 cudaError_t pcg_dispatch(const PcgShape& sh, F&& f) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU;
-  if (sh.threads > 256) return cudaErrorInvalidConfiguration;
+  if (sh.threads > 1024 || sh.bytes > kMaxSmem) return cudaErrorInvalidConfiguration;
+  if (sh.threads > 256) return f(k_pcg<NX, NU, false, false, 1024, 1, 32>);
   if (!sh.smem) return f(k_pcg<NX, NU, false, false, 256, 1>);
   if (sh.minb == 2) return f(k_pcg<NX, NU, true, false, 128, 2>);
   if (sh.lres) return f(k_pcg<NX, NU, true, true, 256, 1>);

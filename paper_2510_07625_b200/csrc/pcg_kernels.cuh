@@ -89,19 +89,33 @@ __device__ __forceinline__ void pcg_finish(const SolveParams& P, int b, int32_t*
   }
 }
 
-// CTA-wide sums with at most 8 warps: xor-shuffle tree, one barrier, fixed tree over the warps
-struct Reducer8 {
-  double2* red;  // [2][8], zero-initialised (slots of absent warps stay zero)
+// CTA-wide sums with at most W warps (8: every kernel of the hot path; 32: the long-horizon build of k_pcg):
+// xor-shuffle tree, one barrier, fixed tree over the warps
+template <int W>
+struct ReducerW {
+  static_assert(W == 8 || W == 32, "warp slots");
+  double2* red;  // [2][W], zero-initialised (slots of absent warps stay zero)
   int flip;
 #ifdef GATO_PCG_TIMING
   long long t_tree = 0, t_bar = 0, t_tail = 0;   // shuffle tree | store + barrier wait | loads + cross-warp tree
 #endif
   __device__ __forceinline__ double2 finish(double2* buf) {
     __syncthreads();
-    const double2 v0 = buf[0], v1 = buf[1], v2 = buf[2], v3 = buf[3], v4 = buf[4], v5 = buf[5], v6 = buf[6],
-                  v7 = buf[7];
-    return make_double2(((v0.x + v1.x) + (v2.x + v3.x)) + ((v4.x + v5.x) + (v6.x + v7.x)),
-                        ((v0.y + v1.y) + (v2.y + v3.y)) + ((v4.y + v5.y) + (v6.y + v7.y)));
+    if constexpr (W == 8) {
+      const double2 v0 = buf[0], v1 = buf[1], v2 = buf[2], v3 = buf[3], v4 = buf[4], v5 = buf[5], v6 = buf[6],
+                    v7 = buf[7];
+      return make_double2(((v0.x + v1.x) + (v2.x + v3.x)) + ((v4.x + v5.x) + (v6.x + v7.x)),
+                          ((v0.y + v1.y) + (v2.y + v3.y)) + ((v4.y + v5.y) + (v6.y + v7.y)));
+    } else {
+      double2 v[W];
+#pragma unroll
+      for (int i = 0; i < W; ++i) v[i] = buf[i];
+#pragma unroll
+      for (int o = 1; o < W; o <<= 1)
+#pragma unroll
+        for (int i = 0; i + o < W; i += 2 * o) v[i] = make_double2(v[i].x + v[i + o].x, v[i].y + v[i + o].y);
+      return v[0];
+    }
   }
   __device__ __forceinline__ double sum1(double a) {
 #ifdef GATO_PCG_TIMING
@@ -109,7 +123,7 @@ struct Reducer8 {
 #endif
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    double2* buf = red + flip * 8;
+    double2* buf = red + flip * W;
     flip ^= 1;
 #ifdef GATO_PCG_TIMING
     const long long c1 = clock64();
@@ -136,7 +150,7 @@ struct Reducer8 {
     keep += __shfl_xor_sync(0xffffffffu, send, 16);
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
-    double2* buf = red + flip * 8;
+    double2* buf = red + flip * W;
     flip ^= 1;
     if ((threadIdx.x & 15) == 0) reinterpret_cast<double*>(buf + (threadIdx.x >> 5))[hi ? 1 : 0] = keep;
     return finish(buf);
@@ -144,16 +158,17 @@ struct Reducer8 {
   __device__ __forceinline__ double max1(double a) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a = nanmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-    double2* buf = red + flip * 8;
+    double2* buf = red + flip * W;
     flip ^= 1;
     if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5].x = a;   // absent warps: 0 <= any |step|
     __syncthreads();
     double m = buf[0].x;
 #pragma unroll
-    for (int w = 1; w < 8; ++w) m = nanmax(m, buf[w].x);
+    for (int w = 1; w < W; ++w) m = nanmax(m, buf[w].x);
     return m;
   }
 };
+using Reducer8 = ReducerW<8>;
 
 template <int NX>
 __device__ __forceinline__ void vec_load(const double* src, double* v) {
@@ -557,14 +572,16 @@ __host__ __device__ constexpr int pcg_threads(int N) { return ((N + 1) + 31) / 3
 // shared memory: reduction slots, the exchange vector, then the O^ blocks (or, when they stay in global
 // memory, the two vectors of the step recovery)
 template <int NX>
-__host__ __device__ constexpr size_t pcg_smem_bytes(int N, bool mats, bool lres = false) {
-  const size_t fixed = 16 * 16 + (size_t)((N + 1) * NX + 2) * 8;
+__host__ __device__ constexpr size_t pcg_smem_bytes(int N, bool mats, bool lres = false, int warp_slots = 8) {
+  const size_t fixed = 2 * (size_t)warp_slots * 16 + (size_t)((N + 1) * NX + 2) * 8;
   const size_t vecs = 2 * (size_t)((N + 1) * NX + 2) * 8;
   const size_t blocks = (size_t)N * PcgLayout<NX>::BSP * 8 + (lres ? (size_t)(N + 1) * PcgLayout<NX>::TRP * 8 : 0);
   return fixed + (mats ? (blocks > vecs ? blocks : vecs) : vecs);
 }
 
-template <int NX, int NU, bool SMEM_MATS, bool LRES, int MAXT, int MINB>
+// MAXT = 1024 (RW = 32 warp slots) is the long-horizon build: N + 1 up to 1024 block rows, matrices in global
+// memory, registers capped at 64 per thread -- slow (spills), but it removes the horizon cap of the fast builds.
+template <int NX, int NU, bool SMEM_MATS, bool LRES, int MAXT, int MINB, int RW = 8>
 __global__ void __launch_bounds__(MAXT, MINB) k_pcg(SolveParams P) {
   constexpr int KPW = 32;
   static_assert(NX % 2 == 0 && (SMEM_MATS || !LRES), "state = [positions, velocities]; L resident only beside O^");
@@ -580,14 +597,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_pcg(SolveParams P) {
   extern __shared__ __align__(16) double pcg_smem[];
   const int vlen = nb * NX;
   double2* red = reinterpret_cast<double2*>(pcg_smem);
-  double* xv = reinterpret_cast<double*>(red + 16);     // exchange vector, nb slots of NX
+  double* xv = reinterpret_cast<double*>(red + 2 * RW);     // exchange vector, nb slots of NX
   double* mats = xv + vlen + 2;
   double* pm = P.pmats + (size_t)b * L::mat_doubles(N);
   const double* LiG = pm + (size_t)N * L::BSP;            // packed L_k^-1 (global)
   const double* LfG = LiG + (size_t)nb * L::TRP;          // packed L_k (global)
   __shared__ __align__(8) unsigned long long fill_bar;
   const unsigned bar = (unsigned)__cvta_generic_to_shared(&fill_bar);
-  if (t < 16) red[t] = make_double2(0.0, 0.0);
+  if (t < 2 * RW) red[t] = make_double2(0.0, 0.0);
   if constexpr (SMEM_MATS) {
     if (t == 0) mbar_init(bar);
   }
@@ -609,7 +626,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_pcg(SolveParams P) {
   const int k = valid ? krow : 0;
   constexpr int row0 = 0;
   const bool has_blk = valid && k < N;
-  Reducer8 R{red, 0};
+  ReducerW<RW> R{red, 0};
 
   double lam[NX], r[NX], p[NX];
   double g2 = 0.0, viol_part = 0.0;

@@ -233,11 +233,13 @@ def test_random_instances_over_the_model_pool_match_the_oracle(seed):
     assert np.max(np.abs(got[:upto, 5] - want[:upto, 5])) <= 1
 
 
-@pytest.mark.parametrize("M,N", [(1, 1), (3, 2), (5, 3), (7, 35), (2, 36), (3, 64), (2, 65), (1, 255), (33, 5)])
+@pytest.mark.parametrize("M,N", [(1, 1), (3, 2), (5, 3), (7, 35), (2, 36), (3, 64), (2, 65), (1, 255), (33, 5),
+                                  (2, 256), (1, 400), (1, 680)])
 def test_boundary_horizons_match_the_compiled_oracle(M, N):
     """Shortest horizons, the last horizon of the row-resident PCG kernel (N=35), the first and last of the
-    quadrant-resident kernel (N=36, N=64), the first of the fat-thread kernel (N=65) and the longest
-    supported one (N+1 = 256 block rows), iiwa14, against the
+    quadrant-resident kernel (N=36, N=64), the first of the fat-thread kernel (N=65), its last (N+1 = 256 block
+    rows) and the long-horizon build beyond it (N = 256, 400, 680: 1024 threads, 32 warp slots in the reductions;
+    the reference has no horizon cap, blocktri.py:78-81), iiwa14, against the
     compiled C oracle: trajectories and per-iteration PCG counts."""
     from oracle import trajopt_c as oc
     from oracle import trajopt_np as orc
@@ -406,3 +408,11 @@ def test_fused_and_unfused_solves_share_a_batch():
     finally:
         eng.close()
         one.close()
+
+
+def test_horizon_beyond_the_long_build_is_rejected_with_a_message():
+    """N + 1 > 1024 block rows (or exchange vectors beyond shared memory) is refused at engine creation, loudly."""
+    with pytest.raises(RuntimeError, match="horizon too long|kernel set-up failed"):
+        gb.BatchEngine(gb.Iiwa14(), 1, 1024, 0.02, workloads.fixed_budget_settings(1))
+    with pytest.raises(RuntimeError, match="horizon too long|kernel set-up failed"):
+        gb.BatchEngine(gb.Iiwa14(), 1, 900, 0.02, workloads.fixed_budget_settings(1))
