@@ -220,3 +220,42 @@ def test_every_solve_of_the_baseline_batches_matches_the_compiled_oracle(M, N, h
     assert np.array_equal(got.trace[:, :, _lib.TRACE_ALPHA], trace[:, :, 2])
     assert np.array_equal(got.trace[:, :, _lib.TRACE_ACCEPTED], trace[:, :, 5])
     assert rel_inf(got.trace[:, :, _lib.TRACE_MERIT], trace[:, :, 0]) <= 1e-8
+
+
+def test_more_configurations_than_the_engine_cache_holds():
+    """batch_solve with more homogeneous groups (here: 20 timesteps) than the engine cache has slots (16): eviction
+    is least-recently-used and never closes an engine the running call still has work on (the old
+    popitem() closed the newest engine and lost the batch)."""
+    import dataclasses as dc
+    from paper_2510_07625_b200 import batch as gbatch
+    gbatch.clear_engine_cache()
+    cost = gb.CostSpec(Q=np.diag([1.0, 0.1]), R=np.diag([0.01]), QN=np.diag([100.0, 10.0]), goal=np.array([np.pi, 0.0]))
+    base = gb.ProblemSpec(model=gb.Pendulum(), cost=cost, horizon=8, timestep=0.05, x_start=np.zeros(2))
+    problems = [dc.replace(base, timestep=0.03 + 0.002 * i) for i in range(20)]
+    zero = (np.zeros((9, 2)), np.zeros((8, 1)))
+    st = gb.SolverSettings(max_sqp_iterations=3, step_tolerance=None)
+    out = gb.batch_solve(gb.BatchSpec(problems, [zero] * 20, st))
+    assert out.ok and all(r is not None and len(r.trace) == 3 for r in out.results)
+    for i in (0, 7, 19):      # each slot equals its single solve
+        single = gb.sqp_solve(problems[i], *zero, st)
+        assert np.array_equal(single.X, out.results[i].X)
+    assert len(gbatch._ENGINES) <= 20
+    again = gb.batch_solve(gb.BatchSpec(problems[:4], [zero] * 4, st))     # after the call the cache shrinks on demand
+    assert again.ok and len(gbatch._ENGINES) <= 20
+    gbatch.clear_engine_cache()
+
+
+def test_a_problem_that_cannot_be_packed_fails_alone():
+    """batch.py:92-99: an exception raised for one problem (here: an initial trajectory of the wrong size and a
+    force of the wrong dimension) is that slot's error string; the rest of the batch is solved."""
+    cost = gb.CostSpec(Q=np.diag([1.0, 0.1]), R=np.diag([0.01]), QN=np.diag([100.0, 10.0]), goal=np.array([np.pi, 0.0]))
+    good = gb.ProblemSpec(model=gb.Pendulum(), cost=cost, horizon=8, timestep=0.05, x_start=np.zeros(2))
+    zero = (np.zeros((9, 2)), np.zeros((8, 1)))
+    bad_init = (np.zeros((7, 2)), np.zeros((8, 1)))
+    st = gb.SolverSettings(max_sqp_iterations=3, step_tolerance=None)
+    out = gb.batch_solve(gb.BatchSpec([good, good, good], [zero, bad_init, zero], st))
+    assert out.results[0] is not None and out.results[2] is not None and out.results[1] is None
+    assert out.errors[0] is None and out.errors[2] is None
+    assert out.errors[1].startswith("ValueError: cannot reshape array of size 14 into shape (9,2)")
+    assert np.array_equal(out.results[0].X, out.results[2].X)
+    gb.batch.clear_engine_cache()
