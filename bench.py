@@ -401,11 +401,11 @@ class GpuArm:
         eng = self.eng
         with self.torch.cuda.stream(self.stream):
             if self.track:
-                eng.mpc_advance(self.ref_dev, s)    # one kernel: measured state, device shift, goal window
+                eng.mpc_step(self.ref_dev, s)       # ONE launch: measured state, device shift, goal window + the solve
             else:
                 eng.dev["X"].copy_(self.X0)
                 eng.dev["U"].copy_(self.U0)
-            eng.launch()
+                eng.launch()
 
     def device_run(self, warmup, steps, flush, clocks=None, barrier=None):
         """K timed steps, CUDA events per step on the launching stream, L2 flushed between steps (untimed).
@@ -574,7 +574,7 @@ def measure_config(name, w, M, lo, device_index, steps, warmup, flush, fp64_peak
     arm = GpuArm(name, w, M, lo, device_index)
     try:
         dev_ms, wall_s, res_last = arm.device_run(warmup, steps, flush, clocks=clocks, barrier=barrier)
-        launches = arm.eng.launch_count() + (1 if arm.track else 0)   # + k_mpc_advance
+        launches = arm.eng.launch_count()   # the control step's shift / goal window ride in the solve's first kernel
         e2e_s, lat, h2d, d2h = arm.e2e_run(warmup, steps, barrier=barrier)
         kern_ms, P_prof = arm.profile()
         if reduce_max:

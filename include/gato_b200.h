@@ -142,6 +142,14 @@ int gato_create(const gato_config* cfg, gato_handle** out);
 int gato_bind(gato_handle* h, const gato_buffers* bufs);
 /* Runs every solve of the batch to termination, entirely on the device. */
 int gato_solve(gato_handle* h, void* stream);
+/* gato_solve with the warm-start preparation of a control step folded into the solve's first kernel (no launch of
+ * its own; in the graph loop modes the first node's arguments are patched per call):
+ *   shift_mode 0  plain gato_solve
+ *   shift_mode 1  X, U shifted one knot left with the tail duplicated (gato_shift_warm_start), then the solve
+ *   shift_mode 2  gato_mpc_advance(goal_path, path_len, path_stride, step), then the solve
+ * One control period of _MpcEngine.advance (mpc.py:240-274) in a single launch. */
+int gato_solve_mpc(gato_handle* h, void* stream, int32_t shift_mode, const double* goal_path, int64_t path_len,
+                   int64_t path_stride, int64_t step);
 /* X <- [X[1:], X[-1]], U <- [U[1:], U[-1]] for every solve, in place (mpc.py:85-89). */
 int gato_shift_warm_start(gato_handle* h, void* stream);
 /* One control period of a device-resident MPC loop (mpc.py:240-274), in place on the bound buffers:

@@ -47,6 +47,7 @@ EXPORTS = {
     "gato_create": (C.c_int, [C.POINTER(GatoConfig), C.POINTER(C.c_void_p)]),
     "gato_bind": (C.c_int, [C.c_void_p, C.POINTER(GatoBuffers)]),
     "gato_solve": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gato_solve_mpc": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int64, C.c_int64]),
     "gato_shift_warm_start": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gato_solve_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_int64]),

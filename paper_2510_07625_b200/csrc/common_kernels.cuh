@@ -5,37 +5,64 @@
 namespace gato {
 
 // -----------------------------------------------------------------------------------------
-// k_init: per-solve state (sqp.py:222-229).  merit_current is filled by the first pass: its line
-// search carries an extra alpha = 0 candidate (k_linesearch) that k_update reads.
+// k_prologue: per-solve state words (sqp.py:222-229; merit_current is filled by the first pass, whose line search
+// carries an extra alpha = 0 candidate that k_update reads) with the warm-start preparation of a control step
+// folded in, one CTA per solve
+// (the first node of the solve's graph; its arguments are patched per launch):
+//   mode 0  state words only                                               (sqp.py:222-229)
+//   mode 1  X, U shifted one knot left, tail duplicated, then the state words (mpc.py:85-89: gato_solve_host)
+//   mode 2  x_start <- X[1], the shift, goal[k] <- path[min(step + k, path_len - 1)], then the state words
+//           (one control period of a device-resident MPC loop, mpc.py:240-274: gato_solve_mpc)
+// Dynamic shared memory: (N + 1) nx + N nu doubles (staging of the shift).
 // -----------------------------------------------------------------------------------------
-__global__ void k_init(SolveParams P) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b == 0) {
-    P.counters[0] = 0;
-    P.counters[1] = 0;
-    P.counters[2] = (unsigned)P.M;
-    P.counters[3] = 0;
-    P.counters[4] = 0;
-  }
-  if (b >= P.M) return;
-  P.sd[b * SD_WORDS + SD_RHO] = P.rho_init[b];
-  P.sd[b * SD_WORDS + SD_MERIT] = 0.0;
-  P.sd[b * SD_WORDS + SD_VIOL] = 0.0;
-  P.sd[b * SD_WORDS + SD_STEP_INF] = 0.0;
-  int32_t* si = P.si + b * SI_WORDS;
-  si[SI_ACTIVE] = 1;
-  si[SI_IT] = 0;
-  si[SI_RETRIES] = 0;
-  si[SI_SKIP_LS] = 0;
-  si[SI_PCG_ITS] = 0;
-  si[SI_MERIT_VALID] = 0;
-  si[SI_SCHUR_FAIL] = INT_MAX;
-  int32_t* info = P.info + (size_t)b * GATO_INFO_WORDS;
-#pragma unroll
-  for (int i = 0; i < GATO_INFO_WORDS; ++i) info[i] = 0;
-  info[GATO_INFO_FAIL_KNOT] = -1;
-}
+struct PrologueArgs {
+  int mode;
+  const double* path;
+  long long path_len, path_stride, step;
+};
 
+__global__ void __launch_bounds__(128) k_prologue(SolveParams P, int nx, int nu, PrologueArgs G) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.x, N = P.N;
+  if (G.mode != 0) {
+    double* Xb = P.X + (size_t)b * (N + 1) * nx;
+    double* Ub = P.U + (size_t)b * N * nu;
+    const int nX = (N + 1) * nx, nU = N * nu;
+    for (int i = threadIdx.x; i < nX; i += blockDim.x) sh[i] = Xb[i];
+    for (int i = threadIdx.x; i < nU; i += blockDim.x) sh[nX + i] = Ub[i];
+    __syncthreads();
+    if (G.mode == 2) {
+      double* xs = const_cast<double*>(P.x_start) + (size_t)b * nx;
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) xs[i] = sh[nx + i];
+    }
+    for (int i = threadIdx.x; i < nX; i += blockDim.x) Xb[i] = sh[(i + nx < nX) ? i + nx : i];
+    for (int i = threadIdx.x; i < nU; i += blockDim.x) Ub[i] = sh[nX + ((i + nu < nU) ? i + nu : i)];
+    if (G.mode == 2 && G.path) {
+      const double* pb = G.path + (size_t)b * G.path_stride;
+      double* gb = const_cast<double*>(P.goal) + (size_t)b * nX;
+      for (int i = threadIdx.x; i < nX; i += blockDim.x) {
+        long long row = G.step + i / nx;
+        if (row > G.path_len - 1) row = G.path_len - 1;
+        gb[i] = pb[row * nx + i % nx];
+      }
+    }
+  }
+  if (b == 0 && threadIdx.x < 5) P.counters[threadIdx.x] = (threadIdx.x == 2) ? (unsigned)P.M : 0u;
+  if (threadIdx.x == 0) {
+    P.sd[b * SD_WORDS + SD_RHO] = P.rho_init[b];
+    P.sd[b * SD_WORDS + SD_MERIT] = 0.0;
+    P.sd[b * SD_WORDS + SD_VIOL] = 0.0;
+    P.sd[b * SD_WORDS + SD_STEP_INF] = 0.0;
+  }
+  if (threadIdx.x < SI_WORDS) {
+    const int wd = threadIdx.x;
+    P.si[b * SI_WORDS + wd] = (wd == SI_ACTIVE) ? 1 : (wd == SI_SCHUR_FAIL) ? INT_MAX : 0;
+  }
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + GATO_INFO_WORDS) {
+    const int wd = threadIdx.x - 32;
+    P.info[(size_t)b * GATO_INFO_WORDS + wd] = (wd == GATO_INFO_FAIL_KNOT) ? -1 : 0;
+  }
+}
 
 // -----------------------------------------------------------------------------------------
 // k_update: one CTA per solve applies the step (fusing this into the tail of k_linesearch was measured:

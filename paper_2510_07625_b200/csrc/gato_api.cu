@@ -68,6 +68,9 @@ struct gato_handle {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t launches = 0;
   int device = 0;               // the device gato_create ran on: every entry point switches to it
+  cudaGraphNode_t pro_node = nullptr;   // the k_prologue node of the instantiated graph (its arguments are patched per launch)
+  PrologueArgs pro_in_graph = {0, nullptr, 0, 0, 0};
+  size_t pro_smem = 0;
   void* lin_scratch = nullptr;  // model-private linearisation scratch (iiwa14: per-stage link data)
 };
 
@@ -143,10 +146,54 @@ int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond, cudaEvent_t* mark
   return GATO_OK;
 }
 
-int enqueue_prologue(gato_handle* h, cudaStream_t s) {
+int enqueue_prologue(gato_handle* h, cudaStream_t s, const PrologueArgs& a = PrologueArgs{0, nullptr, 0, 0, 0}) {
   const SolveParams& P = h->P;
-  k_init<<<(P.M + 127) / 128, 128, 0, s>>>(P);
+  k_prologue<<<P.M, 128, h->pro_smem, s>>>(P, h->ops.nx, h->ops.nu, a);
   CK(cudaGetLastError());
+  return GATO_OK;
+}
+
+// the k_prologue node of a freshly built graph (root level), so that its arguments can be patched per launch
+int find_prologue_node(gato_handle* h) {
+  h->pro_node = nullptr;
+  size_t n = 0;
+  CK(cudaGraphGetNodes(h->graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CK(cudaGraphGetNodes(h->graph, nodes.data(), &n));
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp;
+    if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) continue;
+    if (kp.func == reinterpret_cast<void*>(k_prologue)) {
+      h->pro_node = nd;
+      break;
+    }
+  }
+  cudaGetLastError();
+  h->pro_in_graph = PrologueArgs{0, nullptr, 0, 0, 0};
+  return h->pro_node ? GATO_OK : GATO_E_CUDA;
+}
+
+bool same_args(const PrologueArgs& a, const PrologueArgs& b) {
+  return a.mode == b.mode && a.path == b.path && a.path_len == b.path_len && a.path_stride == b.path_stride &&
+         a.step == b.step;
+}
+
+int patch_prologue(gato_handle* h, const PrologueArgs& a) {
+  if (same_args(a, h->pro_in_graph)) return GATO_OK;
+  SolveParams P = h->P;
+  int nx = h->ops.nx, nu = h->ops.nu;
+  PrologueArgs args = a;
+  void* params[4] = {&P, &nx, &nu, &args};
+  cudaKernelNodeParams kp = {};
+  kp.func = reinterpret_cast<void*>(k_prologue);
+  kp.gridDim = dim3((unsigned)P.M);
+  kp.blockDim = dim3(128);
+  kp.sharedMemBytes = (unsigned)h->pro_smem;
+  kp.kernelParams = params;
+  CK(cudaGraphExecKernelNodeSetParams(h->exec, h->pro_node, &kp));
+  h->pro_in_graph = a;
   return GATO_OK;
 }
 
@@ -217,6 +264,10 @@ int build_while_graph(gato_handle* h, cudaStream_t s) {
   cudaGraph_t body_out = nullptr;
   CKC(cudaStreamEndCapture(s, &body_out));
   CKC(cudaGraphInstantiate(&h->exec, h->graph, 0));
+  if (find_prologue_node(h) != GATO_OK) {
+    destroy_graph(h);
+    return GATO_E_CUDA;
+  }
   h->graph_valid = true;
   return GATO_OK;
 }
@@ -232,9 +283,15 @@ int build_unrolled_graph(gato_handle* h, cudaStream_t s) {
   }
   CKC(cudaStreamEndCapture(s, &h->graph));
   CKC(cudaGraphInstantiate(&h->exec, h->graph, 0));
+  if (find_prologue_node(h) != GATO_OK) {
+    destroy_graph(h);
+    return GATO_E_CUDA;
+  }
   h->graph_valid = true;
   return GATO_OK;
 }
+
+int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa);
 
 }  // namespace
 
@@ -343,6 +400,9 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   std::vector<double> alphas(P.C);
   for (int c = 0; c < P.C; ++c) alphas[c] = pow(cfg->beta, -(double)c);
   CK(cudaMemcpy(P.alphas, alphas.data(), P.C * sizeof(double), cudaMemcpyHostToDevice));
+  h->pro_smem = ((size_t)(N + 1) * nx + (size_t)N * nu) * sizeof(double);
+  if (h->pro_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_prologue, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->pro_smem));
   CK(cudaEventCreate(&h->ev0));
   CK(cudaEventCreate(&h->ev1));
   CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
@@ -391,6 +451,24 @@ int gato_bind(gato_handle* h, const gato_buffers* b) {
 int gato_solve(gato_handle* h, void* stream) {
   DeviceGuard guard__(h);
   if (!h) return GATO_E_INVALID;
+  return solve_impl(h, stream, PrologueArgs{0, nullptr, 0, 0, 0});
+}
+
+int gato_solve_mpc(gato_handle* h, void* stream, int32_t shift_mode, const double* goal_path, int64_t path_len,
+                   int64_t path_stride, int64_t step) {
+  DeviceGuard guard__(h);
+  if (!h) return GATO_E_INVALID;
+  if (shift_mode < 0 || shift_mode > 2 || (shift_mode == 2 && goal_path && (path_len < 1 || step < 0 || path_stride < 0))) {
+    set_error(h, "gato_solve_mpc: shift_mode in {0, 1, 2}; with a goal path: path_len >= 1, step >= 0, path_stride >= 0");
+    return GATO_E_INVALID;
+  }
+  return solve_impl(h, stream, PrologueArgs{shift_mode, shift_mode == 2 ? goal_path : nullptr, path_len, path_stride, step});
+}
+
+}  // extern "C"
+
+namespace {
+int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa) {
   if (!h->bound) {
     set_error(h, "gato_solve before gato_bind");
     return GATO_E_UNBOUND;
@@ -420,15 +498,20 @@ int gato_solve(gato_handle* h, void* stream) {
   }
   CK(cudaEventRecord(h->ev0, s));
   if (mode == 1 || mode == 2) {
+    int rc = patch_prologue(h, pa);   // this launch's warm-start preparation (no-op if unchanged)
+    if (rc != GATO_OK) return rc;
     CK(cudaGraphLaunch(h->exec, s));
   } else {
-    int rc = enqueue_prologue(h, s);
+    int rc = enqueue_prologue(h, s, pa);
     for (int it = 0; rc == GATO_OK && it < h->P.max_it; ++it) rc = enqueue_pass(h, s, 0);
     if (rc != GATO_OK) return rc;
   }
   CK(cudaEventRecord(h->ev1, s));
   return GATO_OK;
 }
+}  // namespace
+
+extern "C" {
 
 /* number of solves still active after the last enqueued pass (synchronises the stream).
  * Non-zero only in loop modes 2/3 when a PCG-breakdown retry consumed a pass. */
@@ -528,9 +611,8 @@ int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (in_bytes > 0) CK(cudaMemcpyAsync(dev_in, host_in, (size_t)in_bytes, cudaMemcpyHostToDevice, s));
-  int rc = GATO_OK;
-  if (shift_first) rc = gato_shift_warm_start(h, stream);
-  if (rc == GATO_OK) rc = gato_solve(h, stream);
+  // the shift of the warm start rides in the solve's first kernel (k_prologue mode 1): no launch of its own
+  int rc = solve_impl(h, stream, PrologueArgs{shift_first ? 1 : 0, nullptr, 0, 0, 0});
   if (rc != GATO_OK) return rc;
   if (h->loop_mode != 1) {   // no device-side WHILE: a PCG retry may have used up a pass
     int guard = h->cfg.max_sqp_iterations * (h->cfg.pcg_retry_limit + 1) + 1;
@@ -577,7 +659,7 @@ int64_t gato_launch_count(const gato_handle* h) {
   if (!h) return 0;
   unsigned int c[4] = {0, 0, 0, 0};
   if (cudaMemcpy(c, h->P.counters, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  // k_init + per pass: k_hessinv, linearisation (two kernels for iiwa14), k_schur, PCG, k_linesearch, k_update
+  // k_prologue + per pass: k_hessinv, linearisation (two kernels for iiwa14), k_schur, PCG, k_linesearch, k_update
   // (with the fused Schur + PCG path the PCG step is two launches: the fused and the record-reading build)
   const int per_pass = 5 + (h->ops.lin_scratch_bytes(1) > 0 ? 2 : 1) + (h->P.fused ? 1 : 0);
   return 1 + per_pass * (int64_t)c[3];

@@ -35,9 +35,9 @@ namespace gato {
 // ---- shared pieces ------------------------------------------------------------------------
 
 // factorisation failure reported by k_schur for this solve?  (thread 0 records it)
-// The word is only written by k_init (reset) and k_schur (atomicMin), never in a PCG kernel, so every
+// The word is only written by k_prologue (reset) and k_schur (atomicMin), never in a PCG kernel, so every
 // thread of the CTA reads the same value and the decision is CTA-uniform; record_failure deactivates the
-// solve, so the word is not looked at again before the next k_init.
+// solve, so the word is not looked at again before the next k_prologue.
 __device__ __forceinline__ bool pcg_schur_failed(const SolveParams& P, int b, const int32_t* si) {
   const int key = si[SI_SCHUR_FAIL];
   if (key == INT_MAX) return false;

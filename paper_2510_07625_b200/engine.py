@@ -332,10 +332,7 @@ class BatchEngine:
             self.stream.synchronize()
             return int(bi.item()), float(bm.item())
 
-    def mpc_advance(self, goal_path=None, step: int = 0):
-        """One control period on the device, in place (gato_mpc_advance): x_start <- X[:, 1], X and U
-        shifted (mpc.py:85-89) and, with ``goal_path`` (a CUDA float64 tensor [T, n] shared by all solves or
-        [M, T, n]), the goal window advanced to goal_path[step : step + N + 1] (clamped at the end)."""
+    def _goal_path_args(self, goal_path):
         ptr, plen, stride = None, 0, 0
         if goal_path is not None:
             if not (goal_path.is_cuda and goal_path.dtype == self.torch.float64 and goal_path.is_contiguous()):
@@ -348,8 +345,23 @@ class BatchEngine:
             else:
                 raise ValueError(f"goal_path must have shape (T, {n}) or ({self.M}, T, {n})")
             ptr = C.c_void_p(goal_path.data_ptr())
+        return ptr, plen, stride
+
+    def mpc_advance(self, goal_path=None, step: int = 0):
+        """One control period on the device, in place (gato_mpc_advance): x_start <- X[:, 1], X and U
+        shifted (mpc.py:85-89) and, with ``goal_path`` (a CUDA float64 tensor [T, n] shared by all solves or
+        [M, T, n]), the goal window advanced to goal_path[step : step + N + 1] (clamped at the end)."""
+        ptr, plen, stride = self._goal_path_args(goal_path)
         self._check(self.lib.gato_mpc_advance(self.handle, C.c_void_p(self.stream.cuda_stream), ptr, int(plen),
                                               int(stride), int(step)), "gato_mpc_advance")
+
+    def mpc_step(self, goal_path=None, step: int = 0):
+        """One control period AND its solve in one launch (gato_solve_mpc, shift mode 2): what ``mpc_advance`` does
+        rides in the first kernel of the solve's graph.  Same arguments as ``mpc_advance``; asynchronous like
+        ``launch`` (follow with ``finish`` / ``download``).  ``goal_path=None``: shift and state hand-over only."""
+        ptr, plen, stride = self._goal_path_args(goal_path)
+        self._check(self.lib.gato_solve_mpc(self.handle, C.c_void_p(self.stream.cuda_stream), 2, ptr, int(plen),
+                                            int(stride), int(step)), "gato_solve_mpc")
 
     def shift_warm_start(self):
         """X, U <- shifted one knot left with the tail duplicated, on the device (mpc.py:85-89)."""

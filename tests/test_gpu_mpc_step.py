@@ -168,3 +168,39 @@ def test_mpc_advance_is_the_three_host_steps_in_one_kernel():
             eng.mpc_advance(torch.zeros((3, 7), device="cuda", dtype=torch.float64))
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("loop_mode", [0, 3])
+def test_fused_control_step_equals_advance_then_solve(loop_mode):
+    """gato_solve_mpc (BatchEngine.mpc_step): the control step's state hand-over, shift and goal window ride in the
+    first kernel of the solve.  Over several consecutive control steps it must leave exactly what
+    gato_mpc_advance followed by gato_solve leaves (graph loop mode: the first node's arguments are patched per
+    launch; stream loop mode: passed directly)."""
+    import torch
+    M, N, h = 5, 12, 0.02
+    batch = workloads.iiwa14_track_arrays(M, N, h)
+    st = workloads.fixed_budget_settings(1)
+    rng = np.random.default_rng(3)
+    path = torch.as_tensor(np.cumsum(0.01 * rng.standard_normal((40, 14)), axis=0), device="cuda")
+    a = gb.BatchEngine(gb.Iiwa14(), M, N, h, st, loop_mode=loop_mode)
+    b = gb.BatchEngine(gb.Iiwa14(), M, N, h, st, loop_mode=loop_mode)
+    try:
+        a.upload(batch)
+        b.upload(batch)
+        for e in (a, b):
+            e.launch()
+            e.finish()
+        for s in range(4):
+            a.mpc_advance(path, s)
+            a.launch()
+            a.finish()
+            b.mpc_step(path, s)
+            b.finish()
+            ra, rb = a.download(), b.download()
+            assert np.array_equal(ra.X, rb.X) and np.array_equal(ra.U, rb.U), f"control step {s}"
+            assert np.array_equal(ra.trace, rb.trace, equal_nan=True) and np.array_equal(ra.info, rb.info)
+            assert torch.equal(a.dev["goal"], b.dev["goal"]) and torch.equal(a.dev["x_start"], b.dev["x_start"])
+        assert b.launch_count() == a.launch_count()
+    finally:
+        a.close()
+        b.close()
