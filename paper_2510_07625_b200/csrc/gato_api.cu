@@ -136,7 +136,15 @@ int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond, cudaEvent_t* mark
   else CK(cudaStreamWaitEvent(s, h->ev_join, 0));
   CK(h->ops.schur(P, s));
   if (marks) CK(cudaEventRecord(marks[3], s));
-  CK(h->ops.pcg(P, s));
+  if (P.fused && !marks) {   // the two PCG builds take disjoint solves: side by side
+    CK(cudaEventRecord(h->ev_fork, s));
+    CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    CK(h->ops.pcg(P, s, h->side));
+    CK(cudaEventRecord(h->ev_join, h->side));
+    CK(cudaStreamWaitEvent(s, h->ev_join, 0));
+  } else {
+    CK(h->ops.pcg(P, s, nullptr));
+  }
   if (marks) CK(cudaEventRecord(marks[4], s));
   CK(h->ops.linesearch(P, s));
   if (marks) CK(cudaEventRecord(marks[5], s));

@@ -18,7 +18,9 @@ struct ModelOps {
                            void* scratch, cudaStream_t);
   size_t (*lin_scratch_bytes)(int64_t rows);
   cudaError_t (*schur)(const SolveParams&, cudaStream_t);
-  cudaError_t (*pcg)(const SolveParams&, cudaStream_t);
+  // `side`: with P.fused the record-reading build (the solves with general weights: usually none) goes to this
+  // stream, if given, so that it runs beside the fused build instead of after it (the two take disjoint solves)
+  cudaError_t (*pcg)(const SolveParams&, cudaStream_t, cudaStream_t side);
   cudaError_t (*linesearch)(const SolveParams&, cudaStream_t);
   cudaError_t (*step_rows)(const ModelParams&, double, int64_t, const double*, const double*, const double*,
                            double*, cudaStream_t);
@@ -162,7 +164,7 @@ cudaError_t pcg_dispatch(const PcgShape& sh, F&& f) {
 }
 
 template <class Mdl>
-cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
+cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s, cudaStream_t side) {
   constexpr int NX = Mdl::NX, NU = Mdl::NU;
   if constexpr (NX >= 14) {
     const int qmode = pcg_use_q<Mdl>(P.N);
@@ -170,7 +172,7 @@ cudaError_t launch_pcg(const SolveParams& P, cudaStream_t s) {
     if (qmode == 2 || (qmode == 1 && !rt)) {
       // with P.fused both builds run: every solve is taken by exactly one of them (SI_DIAG), the other exits at once
       if (P.fused) k_pcg_q<NX, NU, true><<<P.M, pcg_q_threads(P.N), pcg_q_smem_bytes<NX>(P.N), s>>>(P);
-      k_pcg_q<NX, NU, false><<<P.M, pcg_q_threads(P.N), pcg_q_smem_bytes<NX>(P.N), s>>>(P);
+      k_pcg_q<NX, NU, false><<<P.M, pcg_q_threads(P.N), pcg_q_smem_bytes<NX>(P.N), (P.fused && side) ? side : s>>>(P);
       return cudaGetLastError();
     }
     if (rt) {
