@@ -528,7 +528,7 @@ class GpuArm:
             "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
             "peak_source": "in-run DFMA probe (gato_measure_fp64_peak); MEASURED_PEAKS.json carries no fp64 figure",
             "launch_ms": fam_ms[dominant] / K, "algorithmic_flops_per_launch": fam_flops[dominant] / K,
-            "traffic": ncu_traffic(self.name, names[dominant]),
+            "traffic": ncu_traffic(self.name, names[dominant].split("<")[0]),
             "hbm": {"achieved": alg_bytes / total_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": alg_bytes / total_s / 1e9 / hbm_peak, "peak_source": hbm_src,
                     "algorithmic_bytes_per_step": alg_bytes},
