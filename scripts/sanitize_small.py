@@ -31,6 +31,35 @@ for N, iters, fused in ((8, 2, None), (40, 1, None), (64, 1, None), (70, 1, None
     eng.best_of_batch()
     print("iiwa14 N", N, "status", res.info[:, 2].tolist(), "pcg", res.trace[:, 0, 4].tolist())
     eng.close()
+# round-2 additions: the 1024-thread long-horizon k_pcg (N = 300), the control step folded into the solve's first
+# kernel (k_prologue modes 1 and 2: step(shift=True) above, mpc_step here), and a fused batch in which one solve has
+# dense weights (k_hessinv's schur_list, k_schur_listed, the record-reading k_pcg_q build on the side stream)
+import torch  # noqa: E402
+
+batch = workloads.iiwa14_reach_arrays(1, 300)
+eng = gb.BatchEngine(gb.Iiwa14(), 1, 300, 0.02, workloads.fixed_budget_settings(1), loop_mode=3)
+res = eng.solve(batch)
+print("iiwa14 N 300 status", res.info[:, 2].tolist(), "pcg", res.trace[:, 0, 4].tolist())
+eng.close()
+batch = workloads.iiwa14_track_arrays(3, 12, 0.02)
+path = torch.as_tensor(np.cumsum(0.01 * np.random.default_rng(3).standard_normal((40, 14)), axis=0), device="cuda")
+eng = gb.BatchEngine(gb.Iiwa14(), 3, 12, 0.02, workloads.fixed_budget_settings(1), loop_mode=3)
+eng.upload(batch)
+eng.launch()
+eng.finish()
+for s in range(2):
+    eng.mpc_step(path, s)
+    eng.finish()
+print("mpc_step status", eng.download().info[:, 2].tolist())
+eng.close()
+batch = workloads.iiwa14_reach_arrays(4, 16)
+G = np.random.default_rng(5).standard_normal((14, 14))
+batch.Q[1] = batch.Q[1] + 0.05 * (G @ G.T)
+batch.R[3] = batch.R[3] + 1e-4 * np.ones((7, 7))
+eng = gb.BatchEngine(gb.Iiwa14(), 4, 16, 0.02, workloads.fixed_budget_settings(2), loop_mode=3, fused=True)
+res = eng.solve(batch)
+print("mixed fused batch status", res.info[:, 2].tolist(), "pcg", res.trace[:, 0, 4].tolist())
+eng.close()
 # the reference's analytic models (k_linearize_simple, small block sizes)
 for name in ("pendulum_n8", "cartpole_n8", "twolink_n8", "di7_n8"):
     g = load_golden(name)
