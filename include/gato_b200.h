@@ -164,7 +164,12 @@ int gato_mpc_advance(gato_handle* h, void* stream, const double* goal_path, int6
  * copy `in_bytes` from (pinned) host memory to `dev_in`, optionally shift the warm start, run the
  * solve to termination, copy `out_bytes` from `dev_out` back to host memory and synchronise the
  * stream. dev_in / dev_out are caller-owned device addresses (typically spans of the buffers bound
- * with gato_bind); either copy may be skipped with 0 bytes. */
+ * with gato_bind); either copy may be skipped with 0 bytes.
+ * Up to GATO_ZERO_COPY_MAX bytes per direction (environment, default 1 MiB, 0 = never) and with host buffers
+ * that are pinned and device-mapped (cudaHostAlloc / torch pin_memory), no copy engine is involved: the solve's
+ * first kernel reads the inputs across PCIe and the last kernel of each pass writes the rows of every finished
+ * solve straight into host_out (when dev_out spans result arrays only; a small copy kernel otherwise).
+ * Pageable memory and larger spans take cudaMemcpyAsync. Same bytes in host_out on every route. */
 int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host_in, int64_t in_bytes,
                     int32_t shift_first, const void* dev_out, void* host_out, int64_t out_bytes);
 /* Merit evaluation alone (sqp.py:111-166): for every solve of the bound batch, the L1 merit of the

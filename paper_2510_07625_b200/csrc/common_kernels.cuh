@@ -19,11 +19,45 @@ struct PrologueArgs {
   int mode;
   const double* path;
   long long path_len, path_stride, step;
+  // gato_solve_host, latency regime: the step's inputs are read straight from the caller's pinned (device-mapped)
+  // host buffer by this kernel's threads -- no copy-engine transfer ahead of the graph.  8-byte words; 0 = none.
+  const double* in_host;
+  double* in_dev;
+  long long in_words;
+  // ... and the results are sent back by k_update (SolveParams::outmap): device alias of the host buffer, the
+  // device span it mirrors, bytes; 0 = none
+  long long out_host, out_dev, out_bytes;
 };
+
+// dst[0..words) = src[0..words) by the whole grid, 16 bytes per access and four accesses in flight per thread (one
+// side is host memory behind PCIe: what counts is how many requests are outstanding, not how many instructions)
+__device__ __forceinline__ void grid_copy_words(double* __restrict__ dst, const double* __restrict__ src,
+                                                long long words) {
+  const long long n16 = words >> 1, stride = (long long)gridDim.x * blockDim.x;
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += 4 * stride) {
+    double2 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (i + j * stride < n16) v[j] = s2[i + j * stride];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (i + j * stride < n16) d2[i + j * stride] = v[j];
+  }
+  if ((words & 1) && blockIdx.x == 0 && threadIdx.x == 0) dst[words - 1] = src[words - 1];
+}
+
+// results of gato_solve_host written straight into the caller's pinned host buffer (posted PCIe writes)
+__global__ void __launch_bounds__(256) k_copy_words(double* __restrict__ dst, const double* __restrict__ src,
+                                                    long long words) {
+  grid_copy_words(dst, src, words);
+}
 
 __global__ void __launch_bounds__(128) k_prologue(SolveParams P, int nx, int nu, PrologueArgs G) {
   extern __shared__ double sh[];
   const int b = blockIdx.x, N = P.N;
+  if (G.in_words > 0) grid_copy_words(G.in_dev, G.in_host, G.in_words);   // nothing below reads this span
   if (G.mode != 0) {
     double* Xb = P.X + (size_t)b * (N + 1) * nx;
     double* Ub = P.U + (size_t)b * N * nu;
@@ -48,6 +82,8 @@ __global__ void __launch_bounds__(128) k_prologue(SolveParams P, int nx, int nu,
     }
   }
   if (b == 0 && threadIdx.x < 5) P.counters[threadIdx.x] = (threadIdx.x == 2) ? (unsigned)P.M : 0u;
+  if (b == 0 && threadIdx.x >= 8 && threadIdx.x < 11)
+    P.outmap[threadIdx.x - 8] = threadIdx.x == 8 ? G.out_host : threadIdx.x == 9 ? G.out_dev : G.out_bytes;
   if (threadIdx.x == 0) {
     P.sd[b * SD_WORDS + SD_RHO] = P.rho_init[b];
     P.sd[b * SD_WORDS + SD_MERIT] = 0.0;

@@ -69,9 +69,18 @@ struct gato_handle {
   int64_t launches = 0;
   int device = 0;               // the device gato_create ran on: every entry point switches to it
   cudaGraphNode_t pro_node = nullptr;   // the k_prologue node of the instantiated graph (its arguments are patched per launch)
-  PrologueArgs pro_in_graph = {0, nullptr, 0, 0, 0};
+  PrologueArgs pro_in_graph = {};
   size_t pro_smem = 0;
   void* lin_scratch = nullptr;  // model-private linearisation scratch (iiwa14: per-stage link data)
+  // gato_solve_host: host buffers already found to be pinned and device-mapped (pointer -> device alias or null)
+  struct HostAlias {
+    const void* host;
+    void* dev;
+  };
+  std::vector<HostAlias> host_alias;
+  bool outmap_live = false;     // the last prologue told k_update to send results to a host buffer
+  bool in_solve_host = false;
+  long long zero_copy_max = 1 << 20;   // bytes per direction up to which kernels move the data (GATO_ZERO_COPY_MAX)
 };
 
 namespace {
@@ -154,7 +163,7 @@ int enqueue_pass(gato_handle* h, cudaStream_t s, int use_cond, cudaEvent_t* mark
   return GATO_OK;
 }
 
-int enqueue_prologue(gato_handle* h, cudaStream_t s, const PrologueArgs& a = PrologueArgs{0, nullptr, 0, 0, 0}) {
+int enqueue_prologue(gato_handle* h, cudaStream_t s, const PrologueArgs& a = PrologueArgs{}) {
   const SolveParams& P = h->P;
   k_prologue<<<P.M, 128, h->pro_smem, s>>>(P, h->ops.nx, h->ops.nu, a);
   CK(cudaGetLastError());
@@ -179,13 +188,14 @@ int find_prologue_node(gato_handle* h) {
     }
   }
   cudaGetLastError();
-  h->pro_in_graph = PrologueArgs{0, nullptr, 0, 0, 0};
+  h->pro_in_graph = PrologueArgs{};
   return h->pro_node ? GATO_OK : GATO_E_CUDA;
 }
 
 bool same_args(const PrologueArgs& a, const PrologueArgs& b) {
   return a.mode == b.mode && a.path == b.path && a.path_len == b.path_len && a.path_stride == b.path_stride &&
-         a.step == b.step;
+         a.step == b.step && a.in_host == b.in_host && a.in_dev == b.in_dev && a.in_words == b.in_words &&
+         a.out_host == b.out_host && a.out_dev == b.out_dev && a.out_bytes == b.out_bytes;
 }
 
 int patch_prologue(gato_handle* h, const PrologueArgs& a) {
@@ -301,6 +311,71 @@ int build_unrolled_graph(gato_handle* h, cudaStream_t s) {
 
 int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa);
 
+// The device-side alias of a pinned, device-mapped host buffer (torch's pin_memory, cudaHostAlloc,
+// cudaHostRegister with the mapped flag), or null: pageable memory and anything else goes through cudaMemcpyAsync.
+// Looked up once per pointer.
+void* device_alias(gato_handle* h, const void* host) {
+  for (const gato_handle::HostAlias& a : h->host_alias)
+    if (a.host == host) return a.dev;
+  void* dev = nullptr;
+  cudaPointerAttributes at = {};
+  if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+    dev = at.devicePointer;
+  cudaGetLastError();
+  if (h->host_alias.size() >= 16) h->host_alias.erase(h->host_alias.begin());
+  h->host_alias.push_back({host, dev});
+  return dev;
+}
+
+// does [p, p + bytes) overlap what k_prologue itself reads or writes besides its state words (the iterate it
+// shifts, rho_init)?  Then the inputs cannot be copied by that same kernel.
+bool prologue_touches(const gato_handle* h, const void* p, int64_t bytes) {
+  const SolveParams& P = h->P;
+  const char* lo = static_cast<const char*>(p);
+  const char* hi = lo + bytes;
+  auto hits = [&](const void* q, size_t n) {
+    const char* a = static_cast<const char*>(q);
+    return a < hi && lo < a + n;
+  };
+  const size_t nx = (size_t)h->ops.nx, nu = (size_t)h->ops.nu, M = (size_t)P.M, N = (size_t)P.N;
+  return hits(P.X, M * (N + 1) * nx * 8) || hits(P.U, M * N * nu * 8) || hits(P.rho_init, M * 8);
+}
+
+// is [p, p + bytes) made of result arrays only (X, U, trace, info: each wholly inside or wholly outside), up to
+// alignment padding between them?  Then k_update can send it row by row.
+bool span_is_results(const gato_handle* h, const void* p, int64_t bytes) {
+  const SolveParams& P = h->P;
+  const char* lo = static_cast<const char*>(p);
+  const char* hi = lo + bytes;
+  const size_t nx = (size_t)h->ops.nx, nu = (size_t)h->ops.nu, M = (size_t)P.M, N = (size_t)P.N;
+  const struct {
+    const void* ptr;
+    size_t bytes;
+  } arrays[4] = {{P.X, M * (N + 1) * nx * 8},
+                 {P.U, M * N * nu * 8},
+                 {P.trace, M * (size_t)P.max_it * GATO_TRACE_WORDS * 8},
+                 {P.info, M * GATO_INFO_WORDS * 4}};
+  int64_t covered = 0;
+  for (const auto& a : arrays) {
+    const char* q = static_cast<const char*>(a.ptr);
+    const bool inside = q >= lo && q + a.bytes <= hi, outside = q + a.bytes <= lo || q >= hi;
+    if (!inside && !outside) return false;
+    if (inside) covered += (int64_t)a.bytes;
+  }
+  const int64_t nf = h->ops.nf;
+  const struct {
+    const void* ptr;
+    size_t bytes;
+  } inputs[7] = {{P.x_start, M * nx * 8},    {P.goal, M * (N + 1) * nx * 8}, {P.Q, M * nx * nx * 8},
+                 {P.R, M * nu * nu * 8},     {P.QN, M * nx * nx * 8},        {P.force, M * N * (size_t)nf * 8},
+                 {P.rho_init, M * 8}};
+  for (const auto& a : inputs) {   // an input array in the span: the caller wants it copied back too
+    const char* q = static_cast<const char*>(a.ptr);
+    if (a.ptr && a.bytes && q < hi && lo < q + a.bytes) return false;
+  }
+  return covered + 4 * 16 >= bytes;   // the rest may only be alignment padding between the arrays
+}
+
 }  // namespace
 
 extern "C" {
@@ -314,6 +389,7 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   gato_handle* h = new gato_handle();
   h->cfg = *cfg;
   if (cudaGetDevice(&h->device) != cudaSuccess) h->device = 0;
+  h->zero_copy_max = env_int("GATO_ZERO_COPY_MAX", 1 << 20);
   *out = h;  // returned even on failure so that gato_last_error is readable; caller destroys
   if (!select_ops(cfg->model_id, cfg->model_params, &h->ops)) {
     set_error(h, "unknown model id or unsupported model dimension");
@@ -393,6 +469,7 @@ int gato_create(const gato_config* cfg, gato_handle** out) {
   ALLOC(pcg_iters, M * P.max_it);
   ALLOC(schur_list, M);
   ALLOC(counters, 8);
+  ALLOC(outmap, 4);
 #undef ALLOC
   if (rc != GATO_OK) return rc;
   {
@@ -459,7 +536,7 @@ int gato_bind(gato_handle* h, const gato_buffers* b) {
 int gato_solve(gato_handle* h, void* stream) {
   DeviceGuard guard__(h);
   if (!h) return GATO_E_INVALID;
-  return solve_impl(h, stream, PrologueArgs{0, nullptr, 0, 0, 0});
+  return solve_impl(h, stream, PrologueArgs{});
 }
 
 int gato_solve_mpc(gato_handle* h, void* stream, int32_t shift_mode, const double* goal_path, int64_t path_len,
@@ -470,7 +547,7 @@ int gato_solve_mpc(gato_handle* h, void* stream, int32_t shift_mode, const doubl
     set_error(h, "gato_solve_mpc: shift_mode in {0, 1, 2}; with a goal path: path_len >= 1, step >= 0, path_stride >= 0");
     return GATO_E_INVALID;
   }
-  return solve_impl(h, stream, PrologueArgs{shift_mode, shift_mode == 2 ? goal_path : nullptr, path_len, path_stride, step});
+  return solve_impl(h, stream, PrologueArgs{shift_mode, shift_mode == 2 ? goal_path : nullptr, path_len, path_stride, step, nullptr, nullptr, 0, 0, 0, 0});
 }
 
 }  // extern "C"
@@ -483,6 +560,7 @@ int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa) {
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int mode = h->loop_mode;
+  h->outmap_live = pa.out_host != 0;
   if ((mode == 1 || mode == 2) && !h->graph_valid) {
     // graph capture needs a capturable stream; the legacy default stream is not
     cudaStream_t cs = s;
@@ -539,6 +617,11 @@ int gato_resume(gato_handle* h, void* stream, int32_t passes) {
   DeviceGuard guard__(h);
   if (!h || !h->bound) return GATO_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (h->outmap_live && !h->in_solve_host) {
+    // passes enqueued by the caller after a gato_solve_host: its host buffer is no longer ours to write
+    CK(cudaMemsetAsync(h->P.outmap, 0, 3 * sizeof(long long), s));
+    h->outmap_live = false;
+  }
   for (int it = 0; it < passes; ++it) {
     int rc = enqueue_pass(h, s, 0);
     if (rc != GATO_OK) return rc;
@@ -618,9 +701,35 @@ int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host
     return GATO_E_INVALID;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (in_bytes > 0) CK(cudaMemcpyAsync(dev_in, host_in, (size_t)in_bytes, cudaMemcpyHostToDevice, s));
+  // Latency regime (a few hundred KB per direction): a copy-engine transfer costs ~11 us each way, most of it
+  // scheduling; when the host buffers are pinned and device-mapped the kernels move the data themselves -- the
+  // solve's first kernel reads the inputs across PCIe, a small kernel behind the solve writes the results back.
+  PrologueArgs pa{};
+  pa.mode = shift_first ? 1 : 0;
+  const void* in_alias = (in_bytes > 0 && in_bytes % 8 == 0 && in_bytes <= h->zero_copy_max &&
+                          ((uintptr_t)dev_in | (uintptr_t)host_in) % 16 == 0 && !prologue_touches(h, dev_in, in_bytes))
+                             ? device_alias(h, host_in)
+                             : nullptr;
+  if (in_alias) {
+    pa.in_host = static_cast<const double*>(in_alias);
+    pa.in_dev = static_cast<double*>(dev_in);
+    pa.in_words = in_bytes / 8;
+  } else if (in_bytes > 0) {
+    CK(cudaMemcpyAsync(dev_in, host_in, (size_t)in_bytes, cudaMemcpyHostToDevice, s));
+  }
+  void* out_alias = (out_bytes > 0 && out_bytes % 8 == 0 && out_bytes <= h->zero_copy_max &&
+                     ((uintptr_t)dev_out | (uintptr_t)host_out) % 16 == 0)
+                        ? device_alias(h, host_out)
+                        : nullptr;
+  // results: sent by k_update itself when the span is made of result arrays (plus alignment padding) only
+  const bool out_by_update = out_alias && h->P.max_it >= 1 && span_is_results(h, dev_out, out_bytes);
+  if (out_by_update) {
+    pa.out_host = (long long)(uintptr_t)out_alias;
+    pa.out_dev = (long long)(uintptr_t)dev_out;
+    pa.out_bytes = out_bytes;
+  }
   // the shift of the warm start rides in the solve's first kernel (k_prologue mode 1): no launch of its own
-  int rc = solve_impl(h, stream, PrologueArgs{shift_first ? 1 : 0, nullptr, 0, 0, 0});
+  int rc = solve_impl(h, stream, pa);
   if (rc != GATO_OK) return rc;
   if (h->loop_mode != 1) {   // no device-side WHILE: a PCG retry may have used up a pass
     int guard = h->cfg.max_sqp_iterations * (h->cfg.pcg_retry_limit + 1) + 1;
@@ -629,11 +738,23 @@ int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host
       rc = gato_pending(h, stream, &pending);
       if (rc != GATO_OK) return rc;
       if (pending == 0) break;
+      h->in_solve_host = true;
       rc = gato_resume(h, stream, 1);
+      h->in_solve_host = false;
       if (rc != GATO_OK) return rc;
     }
   }
-  if (out_bytes > 0) CK(cudaMemcpyAsync(host_out, dev_out, (size_t)out_bytes, cudaMemcpyDeviceToHost, s));
+  if (out_by_update) {
+    // already on its way
+  } else if (out_alias) {
+    const long long words = out_bytes / 8;
+    const unsigned blocks = (unsigned)((words / 2 + 1023) / 1024);   // 256 threads x four 16-byte accesses
+    k_copy_words<<<blocks ? blocks : 1, 256, 0, s>>>(static_cast<double*>(out_alias), static_cast<const double*>(dev_out),
+                                                     words);
+    CK(cudaGetLastError());
+  } else if (out_bytes > 0) {
+    CK(cudaMemcpyAsync(host_out, dev_out, (size_t)out_bytes, cudaMemcpyDeviceToHost, s));
+  }
   CK(cudaStreamSynchronize(s));
   return GATO_OK;
 }

@@ -43,6 +43,10 @@ struct SolveParams {
   // scratch
   double *A, *B, *e, *grad, *hinv, *Sdiag, *Soff, *Linv, *Lfac, *pmats, *gamma, *gammaw, *lbw, *lam, *dX, *dU, *merits, *viols, *alphas, *sd;
   int32_t *si, *pcg_iters, *schur_list;   // schur_list: solves of this pass that need k_schur (P.fused only)
+  // gato_solve_host, latency regime: [0] device alias of the caller's pinned result buffer (0: none), [1] the
+  // device address it mirrors, [2] bytes -- written by k_prologue per launch, read by k_update, which sends the
+  // rows of every finished solve straight to the host
+  long long* outmap;
   unsigned int* counters;  // [0] arrivals + [1] active count (one 64-bit word), [2] pending solves, [3] passes run, [4] entries of schur_list
 };
 
@@ -1144,7 +1148,7 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
                                              cudaGraphConditionalHandle cond, int use_cond, unsigned n_solves) {
   int32_t* si = P.si + b * SI_WORDS;
   __shared__ double s_alpha;
-  __shared__ int s_accept, s_state[2];
+  __shared__ int s_accept, s_state[2], s_done;
   // the solve's state words as they were when the kernel started, the same for every thread: thread 0 rewrites
   // them further down while other warps may not have looked yet
   if (threadIdx.x == 0) {
@@ -1220,6 +1224,7 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
   // soon as its own state words are final, while the other threads apply the step.
   if (threadIdx.x == 0) {
     const unsigned long long still = si[SI_ACTIVE] ? 1ull : 0ull;
+    s_done = still ? 0 : 1;
     const unsigned long long old =
         atomicAdd(reinterpret_cast<unsigned long long*>(P.counters), (still << 32) + 1ull);
     if ((unsigned)(old & 0xffffffffull) == n_solves - 1) {
@@ -1242,6 +1247,28 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
       double* U = P.U + (size_t)b * nU;
       const double* dU = P.dU + (size_t)b * nU;
       for (int i = threadIdx.x; i < nU; i += blockDim.x) U[i] = __dadd_rn(U[i], __dmul_rn(alpha, dU[i]));
+    }
+  }
+  // Results of a finished solve go straight into the caller's pinned host buffer (posted writes across PCIe) when
+  // gato_solve_host asked for it: no copy-engine transfer, no kernel of its own behind the loop.  A solve that
+  // finished in an earlier pass is simply sent again.
+  const long long host_base = P.outmap[0];   // CTA-uniform
+  if (host_base != 0) {
+    __syncthreads();
+    if (s_done) {
+      const char* dev_base = reinterpret_cast<const char*>(P.outmap[1]);
+      const long long bytes = P.outmap[2];
+      auto send = [&](const void* row, long long words) {
+        const char* a = static_cast<const char*>(row);
+        if (a < dev_base || a + 8 * words > dev_base + bytes) return;
+        const double* src = static_cast<const double*>(row);
+        double* dst = reinterpret_cast<double*>(host_base + (a - dev_base));
+        for (long long i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+      };
+      send(P.X + (size_t)b * (P.N + 1) * nx, (long long)(P.N + 1) * nx);
+      send(P.U + (size_t)b * P.N * nu, (long long)P.N * nu);
+      send(P.trace + (size_t)b * P.max_it * GATO_TRACE_WORDS, (long long)P.max_it * GATO_TRACE_WORDS);
+      send(P.info + (size_t)b * GATO_INFO_WORDS, GATO_INFO_WORDS / 2);
     }
   }
 }

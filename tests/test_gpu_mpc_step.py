@@ -204,3 +204,88 @@ def test_fused_control_step_equals_advance_then_solve(loop_mode):
     finally:
         a.close()
         b.close()
+
+
+def _engine_with_env(monkeypatch, zero_copy_max, *args, **kwargs):
+    if zero_copy_max is None:
+        monkeypatch.delenv("GATO_ZERO_COPY_MAX", raising=False)
+    else:
+        monkeypatch.setenv("GATO_ZERO_COPY_MAX", str(zero_copy_max))
+    return gb.BatchEngine(*args, **kwargs)     # the limit is read in gato_create
+
+
+@pytest.mark.parametrize("loop_mode", [1, 3])
+def test_host_step_moved_by_kernels_equals_the_copy_engine_path(monkeypatch, loop_mode):
+    """gato_solve_host in the latency regime: inputs read from the pinned host buffer by the solve's first kernel,
+    results sent by k_update as each solve finishes.  Same bytes in the host mirror as with cudaMemcpyAsync on both
+    sides -- over consecutive control steps, with solves that finish in different passes (tolerance mode) and one
+    that fails (its rows are sent by the pass that froze it)."""
+    M, N, h = 6, 12, 0.02
+    batch = workloads.iiwa14_track_arrays(M, N, h)
+    batch.Q[4] = -batch.Q[4]                              # FactorizationError: Q_0 not positive definite
+    batch.goal[2] = batch.X[2]                            # already at the goal: exits at once
+    st = gb.SolverSettings(max_sqp_iterations=6)          # tolerance mode, early exits
+    a = _engine_with_env(monkeypatch, 0, gb.Iiwa14(), M, N, h, st, loop_mode=loop_mode)
+    b = _engine_with_env(monkeypatch, None, gb.Iiwa14(), M, N, h, st, loop_mode=loop_mode)
+    try:
+        ra = a.step(batch, fields=INPUT_FIELDS)
+        rb = b.step(batch, fields=INPUT_FIELDS)
+        for s in range(3):
+            for name in ("X", "U", "trace", "info"):
+                assert np.array_equal(getattr(ra, name), getattr(rb, name), equal_nan=True), (s, name)
+            assert ra.info[4, _lib.INFO_STATUS] != 0 and np.any(ra.info[:, _lib.INFO_N_RECORDS] < 6)
+            nxt = gb.PackedBatch(ra.X[:, 1, :].copy(), batch.goal + 0.01 * (s + 1), batch.Q, batch.R, batch.QN,
+                                 batch.force, batch.rho_init, batch.X, batch.U)
+            ra = a.step(nxt, shift=True)
+            rb = b.step(nxt, shift=True)
+        # the device copies agree with what was sent
+        down = b.download()
+        assert np.array_equal(down.X, rb.X) and np.array_equal(down.trace, rb.trace, equal_nan=True)
+        assert np.array_equal(down.info, rb.info)
+    finally:
+        a.close()
+        b.close()
+
+
+def test_host_step_with_a_span_that_is_not_only_results_or_not_pinned(monkeypatch):
+    """Fallbacks of the same call: a result span that also covers input arrays goes through the copy kernel
+    (k_copy_words), pageable host memory through cudaMemcpyAsync -- same bytes either way."""
+    import ctypes as C
+    M, N, h = 3, 8, 0.02
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    st = workloads.fixed_budget_settings(2)
+    eng = _engine_with_env(monkeypatch, None, gb.Iiwa14(), M, N, h, st)
+    try:
+        ref = eng.solve(batch)
+        eng.upload(batch)
+        eng.stream.synchronize()
+        cin, cout = eng._span("x_start", "force"), eng._span("rho_init", "info")   # rho_init, X, U, trace, info
+        base_d = eng.arena.data_ptr()
+
+        def call(host_base):
+            eng._check(eng.lib.gato_solve_host(
+                eng.handle, C.c_void_p(eng.stream.cuda_stream),
+                C.c_void_p(base_d + 8 * cin.start), C.c_void_p(host_base + 8 * cin.start), 8 * (cin.stop - cin.start), 0,
+                C.c_void_p(base_d + 8 * cout.start), C.c_void_p(host_base + 8 * cout.start),
+                8 * (cout.stop - cout.start)), "gato_solve_host")
+
+        eng.pinned.zero_()
+        for name in ("x_start", "goal", "force"):
+            eng.pin_np[name][...] = getattr(batch, name)
+        call(eng.pinned.data_ptr())
+        for name in ("X", "U", "trace", "info"):
+            assert np.array_equal(eng.pin_np[name], getattr(ref, name), equal_nan=True), name
+        assert np.array_equal(eng.pin_np["rho_init"], batch.rho_init)
+        pageable = np.zeros(eng.arena_doubles)
+        for name in ("x_start", "goal", "force"):
+            o, c = eng.offsets[name]
+            pageable[o:o + c] = np.asarray(getattr(batch, name)).reshape(-1)
+        eng.upload(batch)
+        eng.stream.synchronize()
+        call(pageable.ctypes.data)
+        o, c = eng.offsets["X"]
+        assert np.array_equal(pageable[o:o + c].reshape(ref.X.shape), ref.X)
+        o, c = eng.offsets["trace"]
+        assert np.array_equal(pageable[o:o + c].reshape(ref.trace.shape), ref.trace, equal_nan=True)
+    finally:
+        eng.close()
