@@ -199,8 +199,9 @@ int gato_scratch(gato_handle* h, const char* name, void** dev_ptr, int64_t* coun
 int gato_read_scratch(gato_handle* h, const char* name, void* host_dst, int64_t bytes);
 /* number of kernel launches issued by the last gato_solve (graph nodes count per replay) */
 int64_t gato_launch_count(const gato_handle* h);
-/* device time of the last gato_solve in milliseconds, measured with CUDA events on the
- * launching stream; synchronises on the end event */
+/* device time of the last gato_solve / gato_solve_mpc in milliseconds, measured with CUDA events on the
+ * launching stream; synchronises on the end event. gato_solve_host records no events (its caller times the
+ * call); GATO_E_INVALID if the handle has not run a timed solve yet. */
 int gato_last_solve_ms(gato_handle* h, float* ms);
 /* gato_solve with CUDA events between the kernels of every pass (plain stream launches):
  * ms[0..5] = hessinv, linearize, schur, pcg, linesearch, update totals; ms[6] prologue; ms[7] all. */

@@ -80,6 +80,7 @@ struct gato_handle {
   std::vector<HostAlias> host_alias;
   bool outmap_live = false;     // the last prologue told k_update to send results to a host buffer
   bool in_solve_host = false;
+  bool timed_valid = false;     // ev0 / ev1 have been recorded at least once
   long long zero_copy_max = 1 << 20;   // bytes per direction up to which kernels move the data (GATO_ZERO_COPY_MAX)
 };
 
@@ -309,7 +310,7 @@ int build_unrolled_graph(gato_handle* h, cudaStream_t s) {
   return GATO_OK;
 }
 
-int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa);
+int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa, bool timed = true);
 
 // The device-side alias of a pinned, device-mapped host buffer (torch's pin_memory, cudaHostAlloc,
 // cudaHostRegister with the mapped flag), or null: pageable memory and anything else goes through cudaMemcpyAsync.
@@ -553,7 +554,7 @@ int gato_solve_mpc(gato_handle* h, void* stream, int32_t shift_mode, const doubl
 }  // extern "C"
 
 namespace {
-int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa) {
+int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa, bool timed) {
   if (!h->bound) {
     set_error(h, "gato_solve before gato_bind");
     return GATO_E_UNBOUND;
@@ -582,7 +583,7 @@ int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa) {
       h->loop_mode = mode = 3;
     }
   }
-  CK(cudaEventRecord(h->ev0, s));
+  if (timed) CK(cudaEventRecord(h->ev0, s));   // gato_last_solve_ms; the host-buffer call is timed by its caller
   if (mode == 1 || mode == 2) {
     int rc = patch_prologue(h, pa);   // this launch's warm-start preparation (no-op if unchanged)
     if (rc != GATO_OK) return rc;
@@ -592,7 +593,8 @@ int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa) {
     for (int it = 0; rc == GATO_OK && it < h->P.max_it; ++it) rc = enqueue_pass(h, s, 0);
     if (rc != GATO_OK) return rc;
   }
-  CK(cudaEventRecord(h->ev1, s));
+  if (timed) CK(cudaEventRecord(h->ev1, s));
+  h->timed_valid = h->timed_valid || timed;
   return GATO_OK;
 }
 }  // namespace
@@ -729,7 +731,7 @@ int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host
     pa.out_bytes = out_bytes;
   }
   // the shift of the warm start rides in the solve's first kernel (k_prologue mode 1): no launch of its own
-  int rc = solve_impl(h, stream, pa);
+  int rc = solve_impl(h, stream, pa, false);
   if (rc != GATO_OK) return rc;
   if (h->loop_mode != 1) {   // no device-side WHILE: a PCG retry may have used up a pass
     int guard = h->cfg.max_sqp_iterations * (h->cfg.pcg_retry_limit + 1) + 1;
@@ -867,6 +869,10 @@ int gato_measure_fp64_peak(double* tflops) {
 int gato_last_solve_ms(gato_handle* h, float* ms) {
   DeviceGuard guard__(h);
   if (!h || !ms) return GATO_E_INVALID;
+  if (!h->timed_valid) {
+    set_error(h, "gato_last_solve_ms: no gato_solve / gato_solve_mpc on this handle yet (gato_solve_host is not timed)");
+    return GATO_E_INVALID;
+  }
   CK(cudaEventSynchronize(h->ev1));
   CK(cudaEventElapsedTime(ms, h->ev0, h->ev1));
   return GATO_OK;

@@ -158,6 +158,7 @@ class BatchEngine:
             self.pin = {name: view(self.pinned, name) for name in self.layout}
             self.pin_np = {name: t.numpy() for name, t in self.pin.items()}
             self.stream = torch.cuda.Stream(device=self.device)
+            self._step_calls = {}
             cfg = make_config(model, M, N, timestep, settings, loop_mode, stage_arrays, fused)
             handle = C.c_void_p()
             rc = self.lib.gato_create(C.byref(cfg), C.byref(handle))
@@ -249,9 +250,10 @@ class BatchEngine:
             self.pinned[span].copy_(self.arena[span], non_blocking=True)
         self.stream.synchronize()
         ms = C.c_float(0.0)
-        self._check(self.lib.gato_last_solve_ms(self.handle, C.byref(ms)), "gato_last_solve_ms")
+        # device time of the last launch()/mpc_step(); step() (gato_solve_host) is timed by its caller
+        timed = self.lib.gato_last_solve_ms(self.handle, C.byref(ms)) == 0
         return PackedResult(self.pin_np["X"].copy(), self.pin_np["U"].copy(), self.pin_np["trace"].copy(),
-                            self.pin_np["info"].copy(), float(ms.value))
+                            self.pin_np["info"].copy(), float(ms.value) if timed else float("nan"))
 
     def solve(self, batch: PackedBatch) -> PackedResult:
         """The end-to-end call: host inputs in, host results out."""
@@ -269,27 +271,33 @@ class BatchEngine:
         host -> pinned -> device, the warm start is optionally shifted on the device (mpc.py:85-89), the
         solve runs to termination and X, U, trace, info come back.  copy=False returns views of the
         pinned mirror, valid until the next call."""
-        order = [n for n in self.layout if n in fields]
-        idx = [self.layout.index(n) for n in order]
-        if idx != list(range(idx[0], idx[0] + len(idx))):
-            raise ValueError("step(): the uploaded fields must be adjacent in the arena; use upload() + launch()")
+        call = self._step_calls.get(fields) if isinstance(fields, tuple) else None
+        if call is None:           # the argument list of a field set is built once: this is the control loop's call
+            order = [n for n in self.layout if n in fields]
+            idx = [self.layout.index(n) for n in order]
+            if idx != list(range(idx[0], idx[0] + len(idx))):
+                raise ValueError("step(): the uploaded fields must be adjacent in the arena; use upload() + launch()")
+            cin, cout = self._span(order[0], order[-1]), self._span("X", "info")
+            base_d, base_h = self.arena.data_ptr(), self.pinned.data_ptr()
+            head = (self.handle, C.c_void_p(self.stream.cuda_stream), C.c_void_p(base_d + 8 * cin.start),
+                    C.c_void_p(base_h + 8 * cin.start), 8 * (cin.stop - cin.start))
+            tail = (C.c_void_p(base_d + 8 * cout.start), C.c_void_p(base_h + 8 * cout.start),
+                    8 * (cout.stop - cout.start))
+            call = (head, tail)
+            self._step_calls[tuple(fields)] = call
         if batch is not None:      # None: the caller has written the inputs into host_inputs() already
             for name in fields:
                 src = getattr(batch, name)
                 if src.shape != self.shapes[name]:
                     raise ValueError(f"{name}: expected shape {self.shapes[name]}, got {src.shape}")
                 self.pin_np[name][...] = src
-        cin, cout = self._span(order[0], order[-1]), self._span("X", "info")
-        base_d, base_h = self.arena.data_ptr(), self.pinned.data_ptr()
-        self._check(self.lib.gato_solve_host(
-            self.handle, C.c_void_p(self.stream.cuda_stream),
-            C.c_void_p(base_d + 8 * cin.start), C.c_void_p(base_h + 8 * cin.start), 8 * (cin.stop - cin.start),
-            1 if shift else 0,
-            C.c_void_p(base_d + 8 * cout.start), C.c_void_p(base_h + 8 * cout.start), 8 * (cout.stop - cout.start)),
-            "gato_solve_host")
-        get = (lambda a: a.copy()) if copy else (lambda a: a)
-        return PackedResult(get(self.pin_np["X"]), get(self.pin_np["U"]), get(self.pin_np["trace"]),
-                            get(self.pin_np["info"]), float("nan"))
+        rc = self.lib.gato_solve_host(*call[0], 1 if shift else 0, *call[1])
+        if rc != 0:
+            self._check(rc, "gato_solve_host")
+        pin = self.pin_np
+        if copy:
+            return PackedResult(pin["X"].copy(), pin["U"].copy(), pin["trace"].copy(), pin["info"].copy(), float("nan"))
+        return PackedResult(pin["X"], pin["U"], pin["trace"], pin["info"], float("nan"))
 
     def host_inputs(self) -> dict:
         """Writable numpy views of the pinned staging buffers of the inputs (x_start, goal, force, Q, R, QN,
