@@ -124,7 +124,9 @@ def config_dict(name, w, world):
             "sequence": ("MPC: every step starts from the previous step's solution shifted one knot, measured "
                          "state = predicted next state, goal window advanced" if w["kind"] == "track"
                          else "every step solves the batch from its cold initial guess"),
-            "l2": "GPU arm: a 256 MiB buffer is written between timed steps (L2 flushed, untimed)"}
+            "l2": "GPU arm: a 256 MiB buffer is written between timed steps (L2 flushed, untimed)",
+            "timing": "GPU arm: CUDA events recorded by bench.py on the launching stream around every step; the "
+                      "library's own per-launch event pair is switched off (GATO_FLAG_UNTIMED)"}
 
 
 def make_batch(w, M, lo=0, seed_offset=0):
@@ -385,7 +387,7 @@ class GpuArm:
         self.device = torch.device("cuda", device_index)
         self.batch = make_batch(w, M, lo)
         self.eng = gb.BatchEngine(gb.Iiwa14(), M, self.N, self.h, workloads.fixed_budget_settings(self.K, PCG_TOL, PCG_CAP),
-                                  device=device_index, loop_mode=loop_mode)
+                                  device=device_index, loop_mode=loop_mode, timing=False)   # timed by this file's events
         self.stream = self.eng.stream
         self.ref_path = tracking_reference(w, 8192, workloads.SEED) if self.track else None
         self.ref_dev = torch.as_tensor(self.ref_path, device=self.device) if self.track else None

@@ -91,6 +91,10 @@ extern "C" {
 #define GATO_FLAG_FUSED 2   /* form the Schur system inside the PCG kernel wherever that kernel supports it, also for
                                batches below the size from which it pays (default: decided by batch x horizon) */
 
+#define GATO_FLAG_UNTIMED 4 /* gato_solve / gato_solve_mpc record no CUDA events around the launch (two event records cost
+                               ~5 us of device time per launch: a caller that times the stream itself, or does not
+                               time at all, switches them off); gato_last_solve_ms then fails with GATO_E_INVALID */
+
 typedef struct gato_config {
   int32_t abi_version; /* GATO_ABI_VERSION */
   int32_t model_id;

@@ -12,6 +12,7 @@ from .errors import BackendUnavailableError
 ABI_VERSION = 1
 FLAG_UNFUSED = 1      # gato_config.flags: keep form_schur in its own kernel, write the plain stage arrays
 FLAG_FUSED = 2        # gato_config.flags: Schur formation inside the PCG kernel also for small batches
+FLAG_UNTIMED = 4      # gato_config.flags: no CUDA events around the solve's launch (gato_last_solve_ms unavailable)
 INFO_WORDS = 8
 TRACE_WORDS = 8
 (INFO_N_RECORDS, INFO_CONVERGED, INFO_STATUS, INFO_FAIL_ITER, INFO_FAIL_KNOT, INFO_FAIL_BLOCK,

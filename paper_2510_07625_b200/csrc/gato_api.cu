@@ -555,6 +555,7 @@ int gato_solve_mpc(gato_handle* h, void* stream, int32_t shift_mode, const doubl
 
 namespace {
 int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa, bool timed) {
+  if (h->cfg.flags & GATO_FLAG_UNTIMED) timed = false;
   if (!h->bound) {
     set_error(h, "gato_solve before gato_bind");
     return GATO_E_UNBOUND;

@@ -77,7 +77,8 @@ def _torch():
 
 
 def make_config(model, M: int, N: int, timestep: float, settings: SolverSettings,
-                loop_mode: int = 0, stage_arrays: bool = False, fused: bool | None = None) -> _lib.GatoConfig:
+                loop_mode: int = 0, stage_arrays: bool = False, fused: bool | None = None,
+                timing: bool = True) -> _lib.GatoConfig:
     model_id, params = device_model(model)
     cfg = _lib.GatoConfig()
     cfg.abi_version = _lib.ABI_VERSION
@@ -94,6 +95,8 @@ def make_config(model, M: int, N: int, timestep: float, settings: SolverSettings
     cfg.pcg_retry_limit = settings.pcg_retry_limit
     cfg.loop_mode = loop_mode
     cfg.flags = _lib.FLAG_UNFUSED if (stage_arrays or fused is False) else (_lib.FLAG_FUSED if fused else 0)
+    if not timing:
+        cfg.flags |= _lib.FLAG_UNTIMED
     cfg.timestep = float(timestep)
     cfg.pcg_tolerance = settings.pcg.tolerance
     cfg.mu = settings.line_search.mu
@@ -113,8 +116,9 @@ class BatchEngine:
 
     def __init__(self, model, M: int, N: int, timestep: float, settings: SolverSettings,
                  device: int | None = None, loop_mode: int = 0, stage_arrays: bool = False,
-                 fused: bool | None = None):
-        """``stage_arrays=True`` keeps the Schur formation in its own kernel so that ``scratch()`` can read
+                 fused: bool | None = None, timing: bool = True):
+        """``timing=False``: no CUDA events around the solve's launch (they cost ~5 us of device time per launch);
+        ``device_ms`` of the results is then NaN.  ``stage_arrays=True`` keeps the Schur formation in its own kernel so that ``scratch()`` can read
         Sdiag, Soff, Linv, Lfac and the matrix record (stage-by-stage parity tests); by default solves with
         diagonal weights form their Schur system inside the PCG kernel (from batch x horizon ~ 3000 block rows
         on, where it pays; ``fused=True`` / ``False`` forces either path) and those arrays are not written."""
@@ -159,7 +163,7 @@ class BatchEngine:
             self.pin_np = {name: t.numpy() for name, t in self.pin.items()}
             self.stream = torch.cuda.Stream(device=self.device)
             self._step_calls = {}
-            cfg = make_config(model, M, N, timestep, settings, loop_mode, stage_arrays, fused)
+            cfg = make_config(model, M, N, timestep, settings, loop_mode, stage_arrays, fused, timing)
             handle = C.c_void_p()
             rc = self.lib.gato_create(C.byref(cfg), C.byref(handle))
             self.handle = handle

@@ -416,3 +416,19 @@ def test_horizon_beyond_the_long_build_is_rejected_with_a_message():
         gb.BatchEngine(gb.Iiwa14(), 1, 1024, 0.02, workloads.fixed_budget_settings(1))
     with pytest.raises(RuntimeError, match="horizon too long|kernel set-up failed"):
         gb.BatchEngine(gb.Iiwa14(), 1, 900, 0.02, workloads.fixed_budget_settings(1))
+
+
+def test_untimed_engine_gives_the_same_result_without_a_device_time():
+    """GATO_FLAG_UNTIMED (BatchEngine(timing=False)): no event pair around the launch, device_ms is NaN, bits unchanged."""
+    M, N = 3, 10
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    st = workloads.fixed_budget_settings(2)
+    timed = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, st)
+    untimed = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, st, timing=False)
+    try:
+        a, b = timed.solve(batch), untimed.solve(batch)
+    finally:
+        timed.close()
+        untimed.close()
+    assert a.device_ms > 0.0 and np.isnan(b.device_ms)
+    assert np.array_equal(a.X, b.X) and np.array_equal(a.U, b.U) and np.array_equal(a.trace, b.trace, equal_nan=True)
