@@ -454,6 +454,10 @@ class GpuArm:
                                                                    "rho_init", "X", "U")
         h2d = sum(getattr(step_inputs, f).nbytes for f in fields)
         host_in = eng.host_inputs()      # pinned staging buffers of the inputs, written in place
+        mirror = None
+        if not self.track:               # the cold problem batch lives in its own pinned buffer: the engine's mirror
+            mirror = eng.input_mirror()  # receives the results, which overwrite X and U
+            mirror.write(step_inputs, fields)
 
         def step(s):
             if self.track:
@@ -461,9 +465,7 @@ class GpuArm:
                 out = eng.step(None, fields=fields, shift=True, copy=False)
                 host_in["x_start"][...] = out.X[:, 1, :]       # "measured" state for the next control step
             else:
-                for f in fields:
-                    host_in[f][...] = getattr(step_inputs, f)
-                out = eng.step(None, fields=fields, copy=False)
+                out = eng.step(None, fields=fields, copy=False, mirror=mirror)
             return out
 
         for s in range(min(warmup, 5)):

@@ -268,13 +268,22 @@ class BatchEngine:
 
     STEP_FIELDS = ("x_start", "goal", "force")
 
+    def input_mirror(self) -> "InputMirror":
+        """A second pinned staging buffer for the inputs, laid out like the engine's own.  The engine's mirror
+        receives the results, so its X and U are overwritten by every step; a caller that solves from the same
+        (or separately prepared) initial iterate again and again keeps it here and passes it to ``step(mirror=)``."""
+        return InputMirror(self)
+
     def step(self, batch: PackedBatch | None, fields=STEP_FIELDS, shift: bool = False,
-             copy: bool = True) -> PackedResult:
+             copy: bool = True, mirror: "InputMirror | None" = None) -> PackedResult:
         """One control step with host buffers in ONE call across the C ABI (gato_solve_host): the named
         inputs (a contiguous run of the arena; default: the per-step MPC inputs x_start, goal, force) go
         host -> pinned -> device, the warm start is optionally shifted on the device (mpc.py:85-89), the
         solve runs to termination and X, U, trace, info come back.  copy=False returns views of the
-        pinned mirror, valid until the next call."""
+        pinned mirror, valid until the next call.  ``mirror``: read the inputs from this staging buffer
+        (``input_mirror()``) instead of the engine's own."""
+        if mirror is not None:
+            return self._step_from(mirror, batch, fields, shift, copy)
         call = self._step_calls.get(fields) if isinstance(fields, tuple) else None
         if call is None:           # the argument list of a field set is built once: this is the control loop's call
             order = [n for n in self.layout if n in fields]
@@ -302,6 +311,24 @@ class BatchEngine:
         if copy:
             return PackedResult(pin["X"].copy(), pin["U"].copy(), pin["trace"].copy(), pin["info"].copy(), float("nan"))
         return PackedResult(pin["X"], pin["U"], pin["trace"], pin["info"], float("nan"))
+
+    def _step_from(self, mirror, batch, fields, shift, copy):
+        order = [n for n in self.layout if n in fields]
+        idx = [self.layout.index(n) for n in order]
+        if idx != list(range(idx[0], idx[0] + len(idx))):
+            raise ValueError("step(): the uploaded fields must be adjacent in the arena; use upload() + launch()")
+        if batch is not None:
+            mirror.write(batch, fields)
+        cin, cout = self._span(order[0], order[-1]), self._span("X", "info")
+        base_d = self.arena.data_ptr()
+        self._check(self.lib.gato_solve_host(
+            self.handle, C.c_void_p(self.stream.cuda_stream), C.c_void_p(base_d + 8 * cin.start),
+            C.c_void_p(mirror.pinned.data_ptr() + 8 * cin.start), 8 * (cin.stop - cin.start), 1 if shift else 0,
+            C.c_void_p(base_d + 8 * cout.start), C.c_void_p(self.pinned.data_ptr() + 8 * cout.start),
+            8 * (cout.stop - cout.start)), "gato_solve_host")
+        pin = self.pin_np
+        get = (lambda a: a.copy()) if copy else (lambda a: a)
+        return PackedResult(get(pin["X"]), get(pin["U"]), get(pin["trace"]), get(pin["info"]), float("nan"))
 
     def host_inputs(self) -> dict:
         """Writable numpy views of the pinned staging buffers of the inputs (x_start, goal, force, Q, R, QN,
@@ -420,6 +447,27 @@ def _dev(torch, arr, dtype=None):
     if arr.size == 0:        # e.g. the off-diagonal stack of a single-block-row system
         return torch.zeros(1, dtype=torch.float64, device="cuda")
     return torch.as_tensor(arr).cuda()
+
+
+class InputMirror:
+    """Pinned host staging of an engine's inputs (same layout as the engine's own mirror); see
+    ``BatchEngine.input_mirror``."""
+
+    def __init__(self, eng: "BatchEngine"):
+        torch = eng.torch
+        self.shapes = eng.shapes
+        self.pinned = torch.zeros(eng.offsets["U"][0] + eng.offsets["U"][1] + 1, dtype=torch.float64).pin_memory()
+        self.arrays = {}
+        for name in INPUT_FIELDS:
+            o, c = eng.offsets[name]
+            self.arrays[name] = self.pinned[o:o + c].view(eng.shapes[name]).numpy()
+
+    def write(self, batch: PackedBatch, fields=INPUT_FIELDS):
+        for name in fields:
+            src = getattr(batch, name)
+            if src.shape != self.shapes[name]:
+                raise ValueError(f"{name}: expected shape {self.shapes[name]}, got {src.shape}")
+            self.arrays[name][...] = src
 
 
 def measure_fp64_peak() -> float:

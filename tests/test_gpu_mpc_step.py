@@ -289,3 +289,22 @@ def test_host_step_with_a_span_that_is_not_only_results_or_not_pinned(monkeypatc
         assert np.array_equal(pageable[o:o + c].reshape(ref.trace.shape), ref.trace, equal_nan=True)
     finally:
         eng.close()
+
+
+def test_step_from_a_separate_input_mirror_repeats_bitwise():
+    """step(mirror=): the inputs (cold iterate included) come from a second pinned buffer, so the same problem batch
+    can be solved again and again although every step's results overwrite X and U of the engine's own mirror."""
+    M, N = 5, 10
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    eng = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, workloads.fixed_budget_settings(2))
+    try:
+        ref = eng.solve(batch)
+        mirror = eng.input_mirror()
+        mirror.write(batch)
+        for _ in range(3):
+            out = eng.step(None, fields=INPUT_FIELDS, mirror=mirror)
+            assert np.array_equal(out.X, ref.X) and np.array_equal(out.U, ref.U)
+            assert np.array_equal(out.trace, ref.trace, equal_nan=True) and np.array_equal(out.info, ref.info)
+        assert np.array_equal(mirror.arrays["X"], batch.X)      # untouched by the results
+    finally:
+        eng.close()
