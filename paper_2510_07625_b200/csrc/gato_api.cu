@@ -72,12 +72,6 @@ struct gato_handle {
   PrologueArgs pro_in_graph = {};
   size_t pro_smem = 0;
   void* lin_scratch = nullptr;  // model-private linearisation scratch (iiwa14: per-stage link data)
-  // gato_solve_host: host buffers already found to be pinned and device-mapped (pointer -> device alias or null)
-  struct HostAlias {
-    const void* host;
-    void* dev;
-  };
-  std::vector<HostAlias> host_alias;
   bool outmap_live = false;     // the last prologue told k_update to send results to a host buffer
   bool in_solve_host = false;
   bool timed_valid = false;     // ev0 / ev1 have been recorded at least once
@@ -314,17 +308,13 @@ int solve_impl(gato_handle* h, void* stream, const PrologueArgs& pa, bool timed 
 
 // The device-side alias of a pinned, device-mapped host buffer (torch's pin_memory, cudaHostAlloc,
 // cudaHostRegister with the mapped flag), or null: pageable memory and anything else goes through cudaMemcpyAsync.
-// Looked up once per pointer.
-void* device_alias(gato_handle* h, const void* host) {
-  for (const gato_handle::HostAlias& a : h->host_alias)
-    if (a.host == host) return a.dev;
+// Asked on every call (a fraction of a microsecond): a cached answer would outlive the buffer it was given for.
+void* device_alias(const void* host) {
   void* dev = nullptr;
   cudaPointerAttributes at = {};
   if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
     dev = at.devicePointer;
   cudaGetLastError();
-  if (h->host_alias.size() >= 16) h->host_alias.erase(h->host_alias.begin());
-  h->host_alias.push_back({host, dev});
   return dev;
 }
 
@@ -711,7 +701,7 @@ int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host
   pa.mode = shift_first ? 1 : 0;
   const void* in_alias = (in_bytes > 0 && in_bytes % 8 == 0 && in_bytes <= h->zero_copy_max &&
                           ((uintptr_t)dev_in | (uintptr_t)host_in) % 16 == 0 && !prologue_touches(h, dev_in, in_bytes))
-                             ? device_alias(h, host_in)
+                             ? device_alias(host_in)
                              : nullptr;
   if (in_alias) {
     pa.in_host = static_cast<const double*>(in_alias);
@@ -722,7 +712,7 @@ int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host
   }
   void* out_alias = (out_bytes > 0 && out_bytes % 8 == 0 && out_bytes <= h->zero_copy_max &&
                      ((uintptr_t)dev_out | (uintptr_t)host_out) % 16 == 0)
-                        ? device_alias(h, host_out)
+                        ? device_alias(host_out)
                         : nullptr;
   // results: sent by k_update itself when the span is made of result arrays (plus alignment padding) only
   const bool out_by_update = out_alias && h->P.max_it >= 1 && span_is_results(h, dev_out, out_bytes);
