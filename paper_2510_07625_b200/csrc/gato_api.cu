@@ -696,7 +696,8 @@ int gato_solve_host(gato_handle* h, void* stream, void* dev_in, const void* host
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // Latency regime (a few hundred KB per direction): a copy-engine transfer costs ~11 us each way, most of it
   // scheduling; when the host buffers are pinned and device-mapped the kernels move the data themselves -- the
-  // solve's first kernel reads the inputs across PCIe, a small kernel behind the solve writes the results back.
+  // solve's first kernel reads the inputs across PCIe, k_update writes the rows of every finished solve back
+  // (or, for a span that is not made of result arrays only, a small copy kernel behind the solve).
   PrologueArgs pa{};
   pa.mode = shift_first ? 1 : 0;
   const void* in_alias = (in_bytes > 0 && in_bytes % 8 == 0 && in_bytes <= h->zero_copy_max &&
