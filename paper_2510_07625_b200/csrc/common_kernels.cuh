@@ -62,8 +62,20 @@ __global__ void __launch_bounds__(128) k_prologue(SolveParams P, int nx, int nu,
     double* Xb = P.X + (size_t)b * (N + 1) * nx;
     double* Ub = P.U + (size_t)b * N * nu;
     const int nX = (N + 1) * nx, nU = N * nu;
-    for (int i = threadIdx.x; i < nX; i += blockDim.x) sh[i] = Xb[i];
-    for (int i = threadIdx.x; i < nU; i += blockDim.x) sh[nX + i] = Ub[i];
+    // every load of a thread is requested before its first store: one round trip to memory, not one per element
+    for (int i0 = threadIdx.x; i0 < nX + nU; i0 += 8 * blockDim.x) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j * blockDim.x;
+        if (i < nX + nU) v[j] = i < nX ? Xb[i] : Ub[i - nX];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j * blockDim.x;
+        if (i < nX + nU) sh[i] = v[j];
+      }
+    }
     __syncthreads();
     if (G.mode == 2) {
       double* xs = const_cast<double*>(P.x_start) + (size_t)b * nx;
@@ -74,10 +86,20 @@ __global__ void __launch_bounds__(128) k_prologue(SolveParams P, int nx, int nu,
     if (G.mode == 2 && G.path) {
       const double* pb = G.path + (size_t)b * G.path_stride;
       double* gb = const_cast<double*>(P.goal) + (size_t)b * nX;
-      for (int i = threadIdx.x; i < nX; i += blockDim.x) {
-        long long row = G.step + i / nx;
-        if (row > G.path_len - 1) row = G.path_len - 1;
-        gb[i] = pb[row * nx + i % nx];
+      for (int i0 = threadIdx.x; i0 < nX; i0 += 4 * blockDim.x) {
+        double v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + j * blockDim.x;
+          long long row = G.step + i / nx;
+          if (row > G.path_len - 1) row = G.path_len - 1;
+          if (i < nX) v[j] = pb[row * nx + i % nx];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + j * blockDim.x;
+          if (i < nX) gb[i] = v[j];
+        }
       }
     }
   }
