@@ -459,13 +459,16 @@ class GpuArm:
             mirror = eng.input_mirror()  # receives the results, which overwrite X and U
             mirror.write(step_inputs, fields)
 
+        call = eng.bind_step(fields, shift=self.track, mirror=mirror)   # gato_solve_host with its arguments bound
+        goal_in, x_in, path = host_in["goal"], host_in["x_start"], self.ref_path
+
         def step(s):
             if self.track:
-                host_in["goal"][...] = self.ref_path[s:s + N + 1][None]
-                out = eng.step(None, fields=fields, shift=True, copy=False)
-                host_in["x_start"][...] = out.X[:, 1, :]       # "measured" state for the next control step
+                goal_in[...] = path[s:s + N + 1]               # this control step's goal window, every solve
+                out = call()
+                x_in[...] = out.X[:, 1, :]                     # "measured" state for the next control step
             else:
-                out = eng.step(None, fields=fields, copy=False, mirror=mirror)
+                out = call()
             return out
 
         for s in range(min(warmup, 5)):

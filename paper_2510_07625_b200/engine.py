@@ -312,6 +312,32 @@ class BatchEngine:
             return PackedResult(pin["X"].copy(), pin["U"].copy(), pin["trace"].copy(), pin["info"].copy(), float("nan"))
         return PackedResult(pin["X"], pin["U"], pin["trace"], pin["info"], float("nan"))
 
+    def bind_step(self, fields=STEP_FIELDS, shift: bool = False, mirror: "InputMirror | None" = None):
+        """The control loop's call, bound once: returns ``f() -> PackedResult`` (views of the pinned mirror, valid
+        until the next call) that does exactly ``step(None, fields, shift, copy=False, mirror=mirror)`` without
+        rebuilding the argument list -- the inputs are written into ``host_inputs()`` (or the mirror) beforehand."""
+        order = [n for n in self.layout if n in fields]
+        idx = [self.layout.index(n) for n in order]
+        if idx != list(range(idx[0], idx[0] + len(idx))):
+            raise ValueError("step(): the uploaded fields must be adjacent in the arena; use upload() + launch()")
+        cin, cout = self._span(order[0], order[-1]), self._span("X", "info")
+        base_d = self.arena.data_ptr()
+        base_in = (self.pinned if mirror is None else mirror.pinned).data_ptr()
+        args = (self.handle, C.c_void_p(self.stream.cuda_stream), C.c_void_p(base_d + 8 * cin.start),
+                C.c_void_p(base_in + 8 * cin.start), 8 * (cin.stop - cin.start), 1 if shift else 0,
+                C.c_void_p(base_d + 8 * cout.start), C.c_void_p(self.pinned.data_ptr() + 8 * cout.start),
+                8 * (cout.stop - cout.start))
+        fn, check = self.lib.gato_solve_host, self._check
+        pin = self.pin_np
+        result = PackedResult(pin["X"], pin["U"], pin["trace"], pin["info"], float("nan"))
+
+        def call():
+            rc = fn(*args)
+            if rc != 0:
+                check(rc, "gato_solve_host")
+            return result
+        return call
+
     def _step_from(self, mirror, batch, fields, shift, copy):
         order = [n for n in self.layout if n in fields]
         idx = [self.layout.index(n) for n in order]

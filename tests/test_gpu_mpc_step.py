@@ -308,3 +308,26 @@ def test_step_from_a_separate_input_mirror_repeats_bitwise():
         assert np.array_equal(mirror.arrays["X"], batch.X)      # untouched by the results
     finally:
         eng.close()
+
+
+def test_bound_step_is_the_step_call():
+    M, N = 4, 10
+    batch = workloads.iiwa14_reach_arrays(M, N)
+    st = workloads.fixed_budget_settings(1)
+    a = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, st)
+    b = gb.BatchEngine(gb.Iiwa14(), M, N, 0.02, st)
+    try:
+        for e in (a, b):
+            e.solve(batch)
+        call = b.bind_step(shift=True)
+        for s in range(3):
+            for e in (a, b):
+                e.host_inputs()["goal"][...] = batch.goal + 0.01 * (s + 1)
+            ra = a.step(None, shift=True)
+            rb = call()
+            assert np.array_equal(ra.X, rb.X) and np.array_equal(ra.trace, rb.trace, equal_nan=True)
+        with pytest.raises(ValueError):
+            b.bind_step(fields=("x_start", "Q"))
+    finally:
+        a.close()
+        b.close()
