@@ -106,3 +106,36 @@ def test_too_many_breakdowns_fail_the_slot_with_the_reference_message():
         if failures >= 3:
             break
     assert failures >= 1, "no badly scaled problem exhausted the retry limit"
+
+
+@pytest.mark.parametrize("loop_mode", [1, 3])
+def test_retried_and_failed_solves_reach_the_host_buffer_whole(monkeypatch, loop_mode):
+    """The same badly scaled family through the control-step call (gato_solve_host): with results sent by k_update
+    as each solve finishes, a solve that went through PCG-breakdown retries (it stays active across the repeated
+    pass) or that exhausted them (frozen by the PCG kernel, not by k_update) must leave the same bytes in the host
+    mirror as the copy-engine route."""
+    from paper_2510_07625_b200.batch import pack_problems
+    from paper_2510_07625_b200.engine import BatchEngine, INPUT_FIELDS
+    from paper_2510_07625_b200 import _lib
+    st = gb.SolverSettings(max_sqp_iterations=3, step_tolerance=None, rho_init=1e-13, rho_min=0.0, rho_factor=1000.0,
+                           pcg=gb.PcgSettings(tolerance=1e-12))
+    group = [c for c in (badly_scaled(seed) for seed in SEEDS) if c[0].model.name == "pendulum"]
+    problems = [g[0] for g in group]
+    packed = pack_problems(problems, [(g[1], g[2]) for g in group], [st.rho_init] * len(group))
+    M, N = len(group), problems[0].horizon
+    results = []
+    for limit in ("0", None):
+        if limit is None:
+            monkeypatch.delenv("GATO_ZERO_COPY_MAX", raising=False)
+        else:
+            monkeypatch.setenv("GATO_ZERO_COPY_MAX", limit)
+        eng = BatchEngine(problems[0].model, M, N, problems[0].timestep, st, loop_mode=loop_mode)
+        try:
+            results.append(eng.step(packed, fields=INPUT_FIELDS))
+        finally:
+            eng.close()
+    a, b = results
+    for name in ("X", "U", "trace", "info"):
+        assert np.array_equal(getattr(a, name), getattr(b, name), equal_nan=True), name
+    retried = a.trace[:, 0, _lib.TRACE_RHO] > 1.5e-13
+    assert np.any(retried & (a.info[:, _lib.INFO_STATUS] == 0)), "no solve recovered through a retry"
