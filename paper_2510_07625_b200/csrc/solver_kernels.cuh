@@ -1147,6 +1147,7 @@ struct BlockReducer {
 __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx, int nu,
                                              cudaGraphConditionalHandle cond, int use_cond, unsigned n_solves) {
   int32_t* si = P.si + b * SI_WORDS;
+  const long long host_base = P.outmap[0];   // CTA-uniform; asked for first, used last (see the end)
   __shared__ double s_alpha;
   __shared__ int s_accept, s_state[2], s_done;
   // the solve's state words as they were when the kernel started, the same for every thread: thread 0 rewrites
@@ -1252,7 +1253,6 @@ __device__ __forceinline__ void update_solve(const SolveParams& P, int b, int nx
   // Results of a finished solve go straight into the caller's pinned host buffer (posted writes across PCIe) when
   // gato_solve_host asked for it: no copy-engine transfer, no kernel of its own behind the loop.  A solve that
   // finished in an earlier pass is simply sent again.
-  const long long host_base = P.outmap[0];   // CTA-uniform
   if (host_base != 0) {
     __syncthreads();
     if (s_done) {
